@@ -1,0 +1,448 @@
+"""Pins for the oracle (CPU only): the oracle is checked against things other
+than itself -- brute force, closed forms, the paper's tool, the paper's worked
+example, a hand-executed instance, exact rational arithmetic and invariants.
+"""
+import itertools
+import json
+import math
+import os
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from synth import random_graph
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------------------
+# independent brute force: Floyd-Warshall (numpy min-plus), not BFS
+# ---------------------------------------------------------------------------
+def floyd_warshall_sums(V, E):
+    D = np.full((V, V), np.inf)
+    np.fill_diagonal(D, 0.0)
+    for u, v in E:
+        D[u, v] = D[v, u] = 1.0
+    for m in range(V):
+        D = np.minimum(D, D[:, m:m + 1] + D[m:m + 1, :])
+    fin = np.isfinite(D)
+    S = [int(D[i][fin[i]].sum()) for i in range(V)]
+    k = [int(fin[i].sum()) for i in range(V)]
+    return S, k
+
+
+def rand_graph(rng, n, p):
+    return {(u, v) for u in range(n) for v in range(u + 1, n) if rng.random() < p}
+
+
+def test_bfs_vs_floyd_warshall_120_graphs():
+    rng = random.Random(20220722)
+    for t in range(120):
+        n = rng.randint(2, 64)
+        p = rng.choice([0.02, 0.05, 0.1, 0.2, 0.5, 0.9])
+        E = rand_graph(rng, n, p)
+        S_fw, k_fw = floyd_warshall_sums(n, E)
+        S_c, k_c = O.bfs_sums(n, E)
+        S_p, k_p = O.bfs_sums(n, E, use_c=False)
+        assert [int(x) for x in S_c] == S_fw, (t, n, p)
+        assert [int(x) for x in k_c] == k_fw
+        assert [int(x) for x in S_p] == S_fw
+        assert [int(x) for x in k_p] == k_fw
+
+
+# ---------------------------------------------------------------------------
+# closed forms (vertices 0..n-1)
+# ---------------------------------------------------------------------------
+def path(n):
+    return {(i, i + 1) for i in range(n - 1)}
+
+
+def star(n):
+    return {(0, i) for i in range(1, n)}
+
+
+def cycle(n):
+    return path(n) | {(0, n - 1)}
+
+
+def complete(n):
+    return {(u, v) for u in range(n) for v in range(u + 1, n)}
+
+
+def kab(a, b):
+    return {(u, a + w) for u in range(a) for w in range(b)}
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 64, 301])
+def test_path_closed_form(n):
+    E = path(n)
+    S, k = O.bfs_sums(n, E)
+    for i in range(n):
+        assert int(S[i]) == i * (i + 1) // 2 + (n - 1 - i) * (n - i) // 2
+        assert int(k[i]) == n
+    assert sum(int(x) for x in S) == (n - 1) * n * (n + 1) // 3
+    c = O.closeness_wf(n, S, k)
+    assert c[0] == (n - 1) / (n * (n - 1) / 2)          # Eq. 1 at an end vertex
+    assert abs(c[0] - 2.0 / n) < 1e-15
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 10, 100])
+def test_star_closed_form(n):
+    S, k = O.bfs_sums(n, star(n))
+    assert int(S[0]) == n - 1
+    for i in range(1, n):
+        assert int(S[i]) == (2 * n - 3 if n > 2 else 1)
+    c = O.closeness_wf(n, S, k)
+    assert c[0] == 1.0
+    if n > 2:
+        assert abs(c[1] - (n - 1) / (2 * n - 3)) < 1e-15
+
+
+@pytest.mark.parametrize("n", [3, 4, 7, 10, 51, 64])
+def test_cycle_closed_form(n):
+    S, k = O.bfs_sums(n, cycle(n))
+    want = n * n // 4 if n % 2 == 0 else (n * n - 1) // 4
+    assert all(int(x) == want for x in S)
+    res = O.analyze(n, cycle(n))
+    assert res["CH"] == set()                      # vertex-transitive, strict > (Z4)
+    assert O.topk_closeness(res["c"], min(5, n)) == list(range(min(5, n)))
+
+
+@pytest.mark.parametrize("n", [2, 4, 9, 33])
+def test_complete_closed_form(n):
+    res = O.analyze(n, complete(n))
+    assert res["S"] == [n - 1] * n
+    assert res["c"] == [1.0] * n
+    assert res["CH"] == set()
+
+
+@pytest.mark.parametrize("a,b", [(1, 1), (2, 3), (5, 7), (10, 4)])
+def test_complete_bipartite_closed_form(a, b):
+    S, _ = O.bfs_sums(a + b, kab(a, b))
+    for u in range(a):
+        assert int(S[u]) == b + 2 * (a - 1)
+    for w in range(a, a + b):
+        assert int(S[w]) == a + 2 * (b - 1)
+
+
+def test_disjoint_union_components():
+    # K3 + P4 + isolated, shifted labels
+    E = {(0, 1), (1, 2), (0, 2)} | {(3, 4), (4, 5), (5, 6)}
+    V = 8
+    S, k = O.bfs_sums(V, E)
+    assert [int(x) for x in k] == [3, 3, 3, 4, 4, 4, 4, 1]
+    assert [int(x) for x in S] == [2, 2, 2, 6, 4, 4, 6, 0]
+    c = O.closeness_wf(V, S, k)
+    assert c[0] == (2 / 2) * (2 / 7)
+    assert c[7] == 0.0
+
+
+# ---------------------------------------------------------------------------
+# the paper's tool: networkx closeness_centrality, bit-equal
+# ---------------------------------------------------------------------------
+def test_closeness_bit_equal_networkx():
+    nx = pytest.importorskip("networkx")
+    rng = random.Random(7)
+    checked = 0
+    for t in range(60):
+        n = rng.randint(1, 80)
+        E = rand_graph(rng, n, rng.choice([0.01, 0.03, 0.08, 0.3]))
+        G = nx.Graph()
+        G.add_nodes_from(range(n))
+        G.add_edges_from(E)
+        ref = nx.closeness_centrality(G, wf_improved=True)
+        S, k = O.bfs_sums(n, E)
+        c = O.closeness_wf(n, S, k)
+        for u in range(n):
+            assert c[u] == ref[u], (t, u, c[u], ref[u])
+            checked += 1
+    assert checked > 1000
+
+
+# ---------------------------------------------------------------------------
+# SPEC.md worked examples (re-checked against networkx in SURVEY §4)
+# ---------------------------------------------------------------------------
+def test_spec_examples():
+    # SPEC.md:120-122
+    S, k = O.bfs_sums(3, path(3))
+    assert [int(x) for x in S] == [3, 2, 3]
+    assert O.pen_sum(2, *O.bfs_sums(2, set())) == [2, 2]
+    # SPEC.md:129-131
+    assert O.closeness_wf(4, *O.bfs_sums(4, complete(4))) == [1.0] * 4
+    c = O.closeness_wf(3, *O.bfs_sums(3, path(3)))
+    assert c[1] == 1.0 and c[0] == 2 / 3
+    c = O.closeness_wf(4, *O.bfs_sums(4, {(0, 1), (2, 3)}))
+    assert c == [1 / 3] * 4
+    # star S4 -> c(0)=1, leaves 3/5, avg 0.7, CH={0}
+    res = O.analyze(4, star(4))
+    assert res["c"][0] == 1.0 and all(abs(x - 0.6) < 1e-15 for x in res["c"][1:])
+    assert res["CH"] == {0}
+    res = O.analyze(3, set())
+    assert res["c"] == [0.0] * 3 and res["CH"] == set()
+    # P3 + isolated vertex: 4/9, 2/3, 4/9, 0
+    c = O.closeness_wf(4, *O.bfs_sums(4, path(3)))
+    assert c == [(2 / 3) * (2 / 3), (2 / 2) * (2 / 3), (2 / 3) * (2 / 3), 0.0]
+
+
+# ---------------------------------------------------------------------------
+# invariants
+# ---------------------------------------------------------------------------
+def components(V, E):
+    parent = list(range(V))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+    for u, v in E:
+        a, b = find(u), find(v)
+        if a != b:
+            parent[max(a, b)] = min(a, b)
+    return [find(x) for x in range(V)]
+
+
+def test_invariants_random():
+    rng = random.Random(99)
+    for t in range(40):
+        n = rng.randint(2, 120)
+        E = rand_graph(rng, n, rng.choice([0.01, 0.03, 0.1]))
+        S, k = O.bfs_sums(n, E)
+        S = [int(x) for x in S]
+        k = [int(x) for x in k]
+        deg = O.degrees(n, E)
+        assert sum(S) % 2 == 0                              # 2 x Wiener index
+        comp = components(n, E)
+        sizes = {}
+        for x in comp:
+            sizes[x] = sizes.get(x, 0) + 1
+        assert sum(k) == sum(s * s for s in sizes.values())
+        for u in range(n):
+            assert k[u] == sizes[comp[u]]                   # constant on a component
+            assert 2 * (k[u] - 1) - deg[u] <= S[u] <= k[u] * (k[u] - 1) // 2
+        # adding an edge never increases any S on a connected pair's component
+        missing = [(u, v) for u in range(n) for v in range(u + 1, n)
+                   if (u, v) not in E and comp[u] == comp[v]]
+        if missing:
+            e = rng.choice(missing)
+            S2, _ = O.bfs_sums(n, E | {e})
+            assert all(int(a) <= b for a, b in zip(S2, S))
+        # relabelling permutes outputs
+        perm = list(range(n))
+        rng.shuffle(perm)
+        Ep = {tuple(sorted((perm[u], perm[v]))) for u, v in E}
+        Sp, kp = O.bfs_sums(n, Ep)
+        for u in range(n):
+            assert int(Sp[perm[u]]) == S[u] and int(kp[perm[u]]) == k[u]
+
+
+# ---------------------------------------------------------------------------
+# AND aggregation vs an independent numpy implementation
+# ---------------------------------------------------------------------------
+def and_numpy(V, layers):
+    keys = None
+    for E in layers:
+        a = np.array(sorted(E), dtype=np.int64).reshape(-1, 2)
+        kk = a[:, 0] * V + a[:, 1]
+        keys = kk if keys is None else np.intersect1d(keys, kk)
+    return {(int(x // V), int(x % V)) for x in keys}
+
+
+def test_and_aggregate_properties():
+    V = 300
+    rng = random.Random(3)
+    base = rand_graph(rng, V, 0.02)
+    layers = []
+    for i in range(3):
+        keep = {e for e in base if rng.random() < 0.7}
+        extra = rand_graph(rng, V, 0.005)
+        layers.append(keep | extra)
+    A = O.and_aggregate(layers)
+    assert A == and_numpy(V, layers)
+    assert O.and_aggregate([layers[0], layers[0]]) == layers[0]
+    assert O.and_aggregate([layers[0], layers[1]]) == O.and_aggregate([layers[1], layers[0]])
+    assert O.and_aggregate([O.and_aggregate([layers[0], layers[1]]), layers[2]]) == A
+    for E in layers:
+        assert A <= E
+    dA = O.degrees(V, A)
+    for u in range(V):
+        assert dA[u] <= min(O.degrees(V, E)[u] for E in layers)
+    # SPEC.md:52-54
+    assert O.and_aggregate([{(0, 1), (1, 2)}, {(1, 2), (2, 3)}]) == {(1, 2)}
+    assert O.and_aggregate([{(0, 1)}, {(2, 3)}]) == set()
+    assert O.or_aggregate([{(0, 1)}, {(1, 2)}]) == {(0, 1), (1, 2)}
+
+
+def test_canonical_edges():
+    assert O.canonical_edges(3, [(0, 1), (1, 2)]) == {(0, 1), (1, 2)}
+    assert O.canonical_edges(3, [(2, 2)]) == set()
+    assert O.canonical_edges(2, [(0, 1), (0, 1), (1, 0)]) == {(0, 1)}
+    with pytest.raises(ValueError):
+        O.canonical_edges(3, [(0, 3)])
+
+
+# ---------------------------------------------------------------------------
+# exact mean (Z6): fsum / n against exact rational arithmetic
+# ---------------------------------------------------------------------------
+def exact_mean(xs):
+    s = sum((Fraction(x) for x in xs), Fraction(0))
+    return float(s) / len(xs)          # Fraction -> float is correctly rounded
+
+
+def test_mean_fsum_adversarial():
+    rng = random.Random(5)
+    cases = [
+        [1.0] + [2.0 ** -53] * 1000,
+        [2.0 ** -100, 1.0, 2.0 ** -100, 2.0 ** -60] * 50,
+        [rng.random() * 2.0 ** -rng.randint(0, 100) for _ in range(5000)],
+        [1.0 / 3.0] * 999 + [2.0 ** -106],
+        [0.1] * 10,
+    ]
+    def left_to_right(xs):        # Python >= 3.12 sum() is compensated; do it plainly
+        acc = 0.0
+        for x in xs:
+            acc += x
+        return acc / len(xs)
+    for xs in cases:
+        assert O.mean_fsum(xs) == exact_mean(xs)
+    # at least one case where left-to-right summation differs from exact
+    assert any(left_to_right(xs) != exact_mean(xs) for xs in cases)
+    # closeness-shaped values
+    for t in range(20):
+        xs = [rng.randint(1, 10 ** 6) / rng.randint(10 ** 6, 10 ** 12) for _ in range(2000)]
+        assert O.mean_fsum(xs) == exact_mean(xs)
+
+
+# ---------------------------------------------------------------------------
+# composition pins
+# ---------------------------------------------------------------------------
+def layer(V, E):
+    return O.analyze(V, E)
+
+
+def test_cc2_paper_worked_example():
+    # node A has sumDist 9 and 7 in layers 1 and 2 -> estSum 9.
+    # Build a 2-vertex stand-in whose pen sums are (9, 7): use the est rule on
+    # summaries directly, as Alg. 1 consumes only sumDist.
+    r1 = {"V": 3, "pen": [9, 1, 1]}
+    r2 = {"V": 3, "pen": [7, 2, 2]}
+    top, est = O.cc2([r1, r2], 3)
+    assert est[0] == 9 and est[1] == 2
+    assert top == [1, 2, 0]
+
+
+def test_cc1_golden_six_vertex():
+    g = json.load(open(os.path.join(GOLDEN, "cc1_six_vertex.json")))
+    V = g["V"]
+    L1 = O.canonical_edges(V, g["L1"])
+    L2 = O.canonical_edges(V, g["L2"])
+    r1, r2 = layer(V, L1), layer(V, L2)
+    assert r1["S"] == g["S1"] and r2["S"] == g["S2"]
+    assert r1["deg"] == g["deg1"] and r2["deg"] == g["deg2"]
+    assert sorted(r1["CH"]) == g["CH1"] and sorted(r2["CH"]) == g["CH2"]
+    mindeg, ratios = O.degdist_ratios([r1, r2])
+    assert mindeg == g["mindeg"]
+    a1 = math.fsum(ratios[0]) / V
+    a2 = math.fsum(ratios[1]) / V
+    assert a1 == float(Fraction(*g["avg1_num_den"]))
+    assert a2 == float(Fraction(*g["avg2_num_den"]))
+    ranked, nR, R = O.cc1([r1, r2], 10)
+    assert sorted(R) == g["CC1_R"] and nR == 4
+    assert ranked == g["CC1_ranked"]
+    top, est = O.cc2([r1, r2], 3)
+    assert est == g["CC2_est"] and top == g["CC2_top3"]
+    A = O.and_aggregate([L1, L2])
+    assert A == O.canonical_edges(V, g["AND_edges"])
+    ra = layer(V, A)
+    assert ra["S"] == g["AND_S"]
+    assert sorted(ra["CH"]) == g["GT_CH"]
+    assert O.topk_closeness(ra["c"], 3) == g["GT_top3"]
+    assert O.naive([r1, r2], 10)[0] == g["naive"]
+    # symmetric in layer order
+    assert O.cc1([r2, r1], 10)[0] == g["CC1_ranked"]
+
+
+def _three_layers(rng, V, base_p=0.04, keep=0.8, extra=0.004):
+    base = rand_graph(rng, V, base_p)
+    return [{e for e in base if rng.random() < keep} | rand_graph(rng, V, extra) for _ in range(3)]
+
+
+def test_cc2_lower_bound_and_symmetry():
+    rng = random.Random(11)
+    for t in range(15):
+        V = rng.randint(8, 64)
+        Ls = _three_layers(rng, V, base_p=rng.choice([0.05, 0.15, 0.3]))
+        rs = [layer(V, E) for E in Ls]
+        ra = layer(V, O.and_aggregate(Ls))
+        top, est = O.cc2(rs, V)
+        for u in range(V):
+            assert est[u] <= ra["pen"][u]           # distance monotonicity
+        # symmetric in layer order; r-ary max = any pairwise fold
+        assert O.cc2(rs[::-1], V)[0] == top
+        e01 = [max(a, b) for a, b in zip(rs[0]["pen"], rs[1]["pen"])]
+        fold = [max(a, b) for a, b in zip(e01, rs[2]["pen"])]
+        assert fold == est
+
+
+def test_cc2_nested_and_identical_layers():
+    rng = random.Random(12)
+    for t in range(10):
+        V = rng.randint(10, 64)
+        Ey = rand_graph(rng, V, 0.3) | path(V)
+        Ex = {e for e in Ey if rng.random() < 0.6} | path(V)      # E_x ⊆ E_y, connected
+        rx, ry = layer(V, Ex), layer(V, Ey)
+        ra = layer(V, O.and_aggregate([Ex, Ey]))
+        top, est = O.cc2([rx, ry], V)
+        assert est == rx["pen"] == ra["pen"]
+        K = min(10, V)
+        assert top[:K] == O.topk_closeness(ra["c"], K)              # connected: Eq.1 order
+        # identical layers
+        top2, _ = O.cc2([rx, rx], K)
+        assert top2 == O.topk_closeness(rx["c"], K)
+        assert O.naive([rx, rx], V)[2] == rx["CH"]
+
+
+def test_cc1_invariants():
+    rng = random.Random(13)
+    for t in range(15):
+        V = rng.randint(8, 64)
+        Ls = _three_layers(rng, V, base_p=rng.choice([0.08, 0.2]))[:rng.choice([2, 3])]
+        rs = [layer(V, E) for E in Ls]
+        ranked, nR, R = O.cc1(rs, V)
+        common = set.intersection(*[r["CH"] for r in rs])
+        assert common <= R
+        A = O.and_aggregate(Ls)
+        adjA = O.adjacency(V, A)
+        # every added non-hub is a common neighbour of some common hub
+        for v in R - common:
+            assert any(v in adjA[u] for u in common)
+        assert O.cc1(rs[::-1], V)[2] == R
+        assert len(ranked) == nR
+
+
+def test_tie_breaks():
+    V = 12
+    res = O.analyze(V, set())
+    assert O.topk_closeness(res["c"], 5) == [0, 1, 2, 3, 4]
+    rs = [O.analyze(V, cycle(V)), O.analyze(V, cycle(V))]
+    assert O.cc2(rs, 4)[0] == [0, 1, 2, 3]
+    assert O.cc1(rs, 4)[1] == 0                    # CH empty on C_n (strict >)
+
+
+def test_metrics_spec_examples():
+    assert O.jaccard({1, 2, 3}, {2, 3, 4}) == 0.5
+    assert O.jaccard(set(), set()) == 1.0
+    assert O.jaccard({1}, set()) == 0.0
+    assert O.prf1({1, 2}, {2, 3}) == (0.5, 0.5, 0.5)
+    assert O.prf1({1, 2}, {1, 2}) == (1.0, 1.0, 1.0)
+    assert O.prf1(set(), {1}) == (0.0, 0.0, 0.0)
+
+
+def test_synth_generator_deterministic():
+    a = random_graph(500, 2000, seed=3)
+    b = random_graph(500, 2000, seed=3)
+    assert np.array_equal(a, b) and len(a) == 2000
+    assert np.all(a[:, 0] < a[:, 1])
