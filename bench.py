@@ -1,0 +1,398 @@
+"""bench.py -- all-sources BFS closeness on a synthetic HoMLN, one B200 per rank.
+
+A "step" is one pass of the whole hot path over one HoMLN:
+closeness on every layer, then for every layer subset T: AND aggregation,
+closeness of the AND graph, ground-truth top-K, CC2, CC1 and naive
+composition (top-K lists).  Inputs are resident in HBM when the timed region
+starts; L2 is flushed (256 MiB write) before every timed step.
+
+Metric (BASELINE.json): TEPS = W / time with W = sum over every graph whose
+closeness is computed of sum_components k_c * m_c (Graph500-style undirected
+edges; isolated vertices add 0), plus seconds per HoMLN.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
+Multi-GPU (torchrun): replicas only -- each rank runs its own HoMLN (the
+north star fixes one GPU; no collective is invented), "scaling": "weak".
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import build_config  # noqa: E402
+
+L2_FLUSH_BYTES = 256 << 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2207_11662_b200 import Context
+    from paper_2207_11662_b200 import build as B
+
+    if rank == 0:
+        B.build()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    h = build_config(args.config)
+    V, K = h.V, h.K
+    ctx = Context(dev)
+    s = ctx.stream
+    ctx.set_param("bfs_words", args.words)
+    ctx.set_param("timing", 1)
+    host_layers = [torch.from_numpy(L).pin_memory() for L in h.layers]
+    dev_layers = [t.to(f"cuda:{dev}") for t in host_layers]
+    torch.cuda.synchronize()
+    ids_dev = torch.zeros(max(K, 1), dtype=torch.int32, device=f"cuda:{dev}")
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
+
+    # ---- units W per graph (traversal units for TEPS), from one untimed pass
+    ctx.load_layers(V, dev_layers)
+    units = []
+    graph_names = []
+    for i in range(len(h.layers)):
+        r = ctx.closeness(i, want=("k",))
+        d = ctx.degrees(i)
+        units.append(int((r["k"].astype(np.int64) * d.astype(np.int64)).sum() // 2))
+        graph_names.append(f"L{i}")
+    for T in h.subsets:
+        g = ctx.and_aggregate(list(T))
+        r = ctx.closeness(g, want=("k",))
+        d = ctx.degrees(g)
+        units.append(int((r["k"].astype(np.int64) * d.astype(np.int64)).sum() // 2))
+        graph_names.append("AND" + "".join(map(str, T)))
+        ctx.free_graph(g)
+    W_total = sum(units)
+    arcs = []
+    for i in range(len(h.layers)):
+        arcs.append(2 * ctx.graph_info(i)[1])
+
+    def hot_step():
+        for i in range(len(h.layers)):
+            ctx.closeness(i, out={})
+        for T in h.subsets:
+            g = ctx.and_aggregate(list(T))
+            ctx.closeness(g, out={})
+            ctx.topk_closeness(g, K, out=ids_dev)
+            ctx.compose("cc2", list(T), K, out=ids_dev)
+            ctx.compose("cc1", list(T), K, out=ids_dev)
+            ctx.compose("naive", list(T), K, out=ids_dev)
+            ctx.free_graph(g)
+
+    def flush_l2():
+        with torch.cuda.stream(s):
+            flush.fill_(1)
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        hot_step()
+    ctx.sync()
+    ctx.stats(reset=True)
+
+    # ---- timed (device-resident inputs)
+    clk = ClockSampler(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    times = []
+    for _ in range(args.steps):
+        flush_l2()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        hot_step()
+        e1.record(s)
+        times.append((e0, e1))
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = [a.elapsed_time(b) for a, b in times]
+    st = ctx.stats(reset=True)
+    total_ms = float(sum(ms))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = W_total * world / (ms_per_step / 1e3)
+
+    # ---- e2e: host edge lists -> public API -> host results, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h2d = sum(int(t.numel()) * 4 for t in host_layers)
+        d2h = 0
+        e_ms = []
+        for it in range(max(1, args.steps)):
+            flush_l2()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            ctx.load_layers(V, host_layers)                 # H2D from pinned host memory
+            outs = []
+            for i in range(len(h.layers)):
+                ctx.closeness(i, out={})
+            for T in h.subsets:
+                g = ctx.and_aggregate(list(T))
+                ctx.closeness(g, out={})
+                outs.append(ctx.topk_closeness(g, K))       # D2H of every result list
+                outs.append(ctx.compose("cc2", list(T), K)[0])
+                outs.append(ctx.compose("cc1", list(T), K)[0])
+                outs.append(ctx.compose("naive", list(T), K)[0])
+                ctx.free_graph(g)
+            e1.record(s)
+            e1.synchronize()
+            e_ms.append(e0.elapsed_time(e1))
+            d2h = sum(int(o.nbytes) for o in outs)
+        e2e_ms = float(np.mean(e_ms))
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": W_total * world / (e2e_ms / 1e3), "unit": "TEPS", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    # ---- roofline of the MS-BFS kernel
+    import json as _json
+    peaks = {}
+    try:
+        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    n_bfs = max(1, st["bfs_launches"])
+    bfs_ms_avg = st["bfs_ms"] / n_bfs
+    levels_per_launch = st["bfs_levels"] / n_bfs
+    Rb = args.words * 8
+    # SURVEY §8(d) dense-level model per level: 4(V+1) row_ptr + 4A col + 3 R V state;
+    # A = mean arcs over the graphs closed in a step
+    A_mean = float(np.mean(arcs))
+    model_bytes = levels_per_launch * (4 * (V + 1) + 4 * A_mean + 3 * Rb * V)
+    achieved = model_bytes / (bfs_ms_avg / 1e3) / 1e9 if bfs_ms_avg > 0 else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+            "frac": achieved / peak_gbs, "traffic": None, "peak_source": peak_src,
+            "kernel": "msbfs_kernel", "bytes_model": "SURVEY 8(d) dense-level: L*(4(V+1)+4A+3RV)",
+            "bytes_per_launch": model_bytes, "ms_per_launch": bfs_ms_avg,
+            "levels_per_launch": levels_per_launch, "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9)}
+    launches_per_step = st["launches"] / args.steps
+
+    line = {
+        "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",
+        "value": value, "unit": "TEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": h.name, "V": V, "layers": len(h.layers), "subsets": [list(t) for t in h.subsets],
+                   "K": K, "recipe": h.recipe, "units_W": W_total, "units_per_graph": dict(zip(graph_names, units)),
+                   "bfs_words": args.words, "sources_per_batch": 64 * args.words,
+                   "l2": "flushed (256 MiB write) before each timed step", "parallelism": f"replicas{world}"},
+        "s_per_homln": ms_per_step / 1e3,
+        "e2e": e2e, "roofline": roof, "clocks": clocks, "gpu_launches": int(round(launches_per_step)),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(h, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+# ---------------------------------------------------------------------------
+# oracle timing (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------
+def _component_edges(V, E):
+    """per-vertex m_c (edges of its component) -- bookkeeping for the TEPS numerator."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+    E = np.asarray(E, dtype=np.int64).reshape(-1, 2)
+    A = sp.coo_matrix((np.ones(len(E)), (E[:, 0], E[:, 1])), shape=(V, V))
+    nc, lab = connected_components(A, directed=False)
+    m_c = np.bincount(lab[E[:, 0]], minlength=nc)
+    return m_c[lab]
+
+
+def oracle_sample(V, E, seconds, threads, seed=0):
+    """time the oracle's plain per-source BFS on a deterministic source sample
+    sized to about `seconds`; returns (units, seconds, n_sources)."""
+    from oracle import _bfs
+    mcv = _component_edges(V, E)
+    rng = np.random.default_rng(seed)
+    n = 64
+    t_total, u_total, s_total = 0.0, 0, 0
+    while True:
+        src = rng.integers(0, V, size=n).astype(np.int32)
+        t0 = time.perf_counter()
+        _bfs.bfs_sources(V, E, src, threads)
+        dt = time.perf_counter() - t0
+        t_total += dt
+        u_total += int(mcv[src].sum())
+        s_total += n
+        if t_total >= seconds * 0.5 or n >= V:
+            break
+        n = int(min(V, max(n * 2, n * (seconds * 0.5 - t_total) / max(dt, 1e-3))))
+    return u_total, t_total, s_total
+
+
+def cpu_baseline(h, seconds):
+    from oracle import _bfs
+    threads = os.cpu_count() or 1
+    used = _bfs.num_threads(threads)
+    E = h.layers[0]
+    u, t, n = oracle_sample(h.V, E, seconds, threads)
+    return {"value": u / t, "unit": "TEPS", "cores": used, "kind": "oracle",
+            "sample": f"oracle plain per-source BFS from {n} random sources of {h.name} layer 0 "
+                      f"({t:.1f} s, TEPS = sum of m_c over sampled sources / time)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import _bfs
+    from oracle import oracle as O
+    h = build_config(args.config)
+    threads = os.cpu_count() or 1
+    used = _bfs.num_threads(threads)
+    graphs = [L for L in h.layers]
+    for T in h.subsets:
+        A = O.and_aggregate([set(map(tuple, h.layers[i].tolist())) for i in T])
+        graphs.append(np.array(sorted(A), dtype=np.int32).reshape(-1, 2))
+    per = max(1.0, args.cpu_seconds / max(1, len(graphs)))
+
+    def step():
+        u_tot, t_tot, n_tot = 0, 0.0, 0
+        for E in graphs:
+            u, t, n = oracle_sample(h.V, E, per, threads)
+            u_tot += u
+            t_tot += t
+            n_tot += n
+        return u_tot, t_tot, n_tot
+
+    for _ in range(args.warmup):
+        step()
+    U, Tt, N = 0, 0.0, 0
+    for _ in range(args.steps):
+        u, t, n = step()
+        U += u
+        Tt += t
+        N += n
+    val = U / Tt
+    line = {
+        "impl": "reference",
+        "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",
+        "value": val, "unit": "TEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": Tt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": h.name, "V": h.V, "K": h.K, "parallelism": "oracle on host cores"},
+        "cpu_baseline": {"value": val, "unit": "TEPS", "cores": used, "kind": "oracle",
+                         "sample": f"per step: oracle plain BFS from a random source sample of each of the "
+                                   f"{len(graphs)} graphs of {h.name} (~{per:.0f} s each); {N} sources total"},
+        "e2e": {"value": val, "unit": "TEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--words", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

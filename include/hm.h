@@ -1,0 +1,174 @@
+/*
+ * hm.h -- C ABI of the B200 (sm_100a) closeness-centrality library for
+ * homogeneous multilayer networks (arXiv 2207.11662, "Closeness Centrality
+ * Detection in Homogeneous Multilayer Networks").
+ *
+ * Problem statement followed (§1): given the layers
+ * G_1(V,E_1) ... G_l(V,E_l) of a HoMLN over one vertex set V, identify the
+ * closeness-centrality (CC) nodes of the Boolean-AND aggregate of any r <= l
+ * layers, from per-layer partial results computed once (the decoupling
+ * approach, §3).
+ *
+ * Every entry point is stream-ordered on the context's CUDA stream.  All
+ * compute runs in this library's own CUDA kernels; there is no CPU fallback.
+ * Pointers called "host or device" are classified with
+ * cudaPointerGetAttributes; host outputs are complete when the call returns,
+ * device outputs are complete in stream order.
+ *
+ * Errors: no exception crosses the ABI.  A non-zero status leaves every output
+ * untouched, stores a message retrievable with hm_last_error(), and leaves the
+ * context usable (except after HM_ECUDA from a sticky device fault).
+ *
+ * Threading: one context is used by one host thread at a time; distinct
+ * contexts are independent.  Results are bit-identical across runs and do not
+ * depend on tuning parameters (hm_set_param).
+ */
+#ifndef HM_H
+#define HM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hm_ctx hm_ctx;      /* opaque: owns device memory and (optionally) a stream */
+typedef int32_t hm_status;
+
+enum {
+    HM_OK = 0,
+    HM_EINVAL = -1,   /* bad argument: V <= 0, l < 1, r < 2, K not in [1, V], null pointer, unknown enum */
+    HM_ERANGE = -2,   /* vertex id outside [0, V), or 2m >= 2^31 arcs (int32 CSR)                          */
+    HM_ENOMEM = -3,   /* device allocation failed                                                          */
+    HM_ECUDA = -4,    /* CUDA runtime / kernel error (message has cudaGetErrorString)                       */
+    HM_ESTATE = -5    /* unknown / freed graph id, compose before closeness, free of a layer              */
+};
+
+enum { HM_NAIVE = 0, HM_CC1 = 1, HM_CC2 = 2 };   /* hm_compose heuristics */
+
+/* ---------------------------------------------------------------- context */
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to
+ * issue all work on (borrowed, e.g. torch.cuda.current_stream().cuda_stream),
+ * or NULL for a context-owned non-blocking stream.  *out receives the context. */
+hm_status hm_create(hm_ctx **out, int device, void *cuda_stream);
+
+/* Release every device buffer and the owned stream.  NULL is a no-op. */
+void hm_destroy(hm_ctx *ctx);
+
+/* Message for the last non-OK status on ctx (owned by ctx; "" if none). */
+const char *hm_last_error(const hm_ctx *ctx);
+
+/* Tuning knobs (results never depend on them):
+ *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16 or 32; sources per batch = 64*words)
+ *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
+ *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (0 = occupancy maximum)
+ *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
+ * Unknown name -> HM_EINVAL. */
+hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value);
+
+/* --------------------------------------------------------------- graphs */
+
+/* Load the l layers of a HoMLN (§1).  Vertices are 0..V-1 in every
+ * layer.  edges[i] points to 2*m[i] int32 values (u0,v0,u1,v1,...), host or
+ * device.  Undirected: either or both directions may be given; self-loops and
+ * duplicates are dropped (count in dropped_out[i] if non-NULL, host array of l).
+ * Builds one CSR per layer on the device (rows ascending).  Assigns graph ids
+ * 0..l-1 in order; replaces any previously loaded HoMLN in ctx.
+ * Errors: V <= 0 or l < 1 -> EINVAL; id outside [0,V) or 2*m[i] >= 2^31 -> ERANGE. */
+hm_status hm_load_layers(hm_ctx *ctx, int32_t V, int32_t l, const int32_t *const *edges,
+                         const int64_t *m, int64_t *dropped_out);
+
+/* Shape and borrowed device views of graph g's CSR (row_ptr: V+1, col: 2m),
+ * valid until g is freed.  Any out pointer may be NULL. */
+hm_status hm_graph_info(hm_ctx *ctx, int32_t g, int32_t *V, int64_t *m_undirected,
+                        const int32_t **d_row_ptr, const int32_t **d_col);
+
+/* Copy graph g's CSR into caller buffers (host or device): row_ptr V+1, col 2m. */
+hm_status hm_graph_csr(hm_ctx *ctx, int32_t g, int32_t *row_ptr, int32_t *col);
+
+/* Boolean AND aggregation (PAPER.md:150 §3.1; :205 §4 ground truth step i):
+ * an edge is in the result iff it is in every one of the r >= 2 distinct graphs
+ * graph_ids[0..r-1] (host array).  Vertex set stays V.  *g_out receives the new
+ * graph id (>= l).  Computed by a sorted-adjacency intersection kernel.
+ * Errors: r < 2 or repeated id -> EINVAL; unknown id -> ESTATE. */
+hm_status hm_and_aggregate(hm_ctx *ctx, const int32_t *graph_ids, int32_t r, int32_t *g_out);
+
+/* Boolean OR aggregation (§3.1): edge in at least one graph. */
+hm_status hm_or_aggregate(hm_ctx *ctx, const int32_t *graph_ids, int32_t r, int32_t *g_out);
+
+/* Release an aggregated graph (ids >= l) and its cached results.  Layers -> ESTATE. */
+hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
+
+/* ------------------------------------------------------------ analysis */
+
+/* All-sources unweighted BFS closeness of graph g (§4; the
+ * analysis function Psi of PAPER.md:121-122).  For every vertex v:
+ *   dist_sum[v]  S(v) = sum of d(v,w) over vertices w reachable from v (uint64)
+ *   reach[v]     k(v) = number of vertices reachable from v, v included
+ *   closeness[v] Wasserman-Faust closeness as NetworkX computes it
+ *                (PAPER.md:186, :209): ((k-1)/S) * ((k-1)/(V-1)) in binary64,
+ *                0 when S == 0 or V <= 1; equals Eq. 1 when k == V
+ *   pen_sum[v]   n-penalty sum sumDist(v) (§5.1): S + (V-k)*V
+ * Also caches, for hm_compose / hm_topk_closeness / hm_cc_nodes: degrees, the
+ * mean closeness mu = (correctly rounded sum of c) / V and the CC-node set
+ * CH = {v : c(v) > mu}.  Any output pointer may be NULL; each
+ * is host or device, length V.  Re-running on a graph recomputes. */
+hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
+                       double *closeness, uint64_t *pen_sum);
+
+/* CC nodes of graph g (needs hm_closeness(g) first, else ESTATE):
+ * bitmap (ceil(V/32) uint32 words, bit v%32 of word v/32; host or device, may
+ * be NULL), *count (may be NULL) and *mean = mu (host, may be NULL). */
+hm_status hm_cc_nodes(hm_ctx *ctx, int32_t g, uint32_t *bitmap, int32_t *count, double *mean);
+
+/* Degrees deg(v) = |NBD(v)| of graph g, V int32, host or device. */
+hm_status hm_degrees(hm_ctx *ctx, int32_t g, int32_t *deg);
+
+/* Ground-truth style ranking: the K vertices of largest
+ * closeness, ties by lower id, in rank order.  1 <= K <= V.  ids_out: K int32,
+ * host or device.  Needs hm_closeness(g) (ESTATE otherwise). */
+hm_status hm_topk_closeness(hm_ctx *ctx, int32_t g, int32_t K, int32_t *ids_out);
+
+/* -------------------------------------------------------- composition */
+
+/* Composition Theta over r >= 2 distinct layer/graph ids (host array), each of
+ * which must have had hm_closeness run (ESTATE otherwise).  Reads only the
+ * cached per-graph results and the graphs' own adjacency (NBD), never the AND
+ * aggregate (the decoupling contract).
+ *   HM_CC2  (Alg. 1): est(v) = max_i pen_i(v); the K
+ *           vertices of largest Eq. 1 score (V-1)/est, i.e. smallest (est, id);
+ *           writes exactly K ids, *count_out = K.
+ *   HM_CC1  (Eq. 2, Eq. 3; pseudocode :477-507; flat r-ary):
+ *           result set R, ranked by RN(est/mindeg) ascending then id; writes
+ *           min(K, |R|) ids, *count_out = |R|.
+ *   HM_NAIVE: intersection of the CC-node sets, ranked by id;
+ *           writes min(K, |R|) ids, *count_out = |R|.
+ * 1 <= K <= V.  ids_out host or device; count_out host (may be NULL). */
+hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, int32_t r,
+                     int32_t K, int32_t *ids_out, int32_t *count_out);
+
+/* ------------------------------------------------------------ utilities */
+
+/* Wait for all work issued on the context stream. */
+hm_status hm_sync(hm_ctx *ctx);
+
+/* Counters since the last reset (reset=1 zeroes them after reading):
+ *   launches       number of this library's kernel launches
+ *   bfs_launches   launches of the persistent MS-BFS kernel
+ *   bfs_ms         summed CUDA-event time of those launches (needs param timing=1)
+ *   bfs_levels     BFS levels executed (sum over batches)
+ *   bfs_batches    source batches executed */
+typedef struct {
+    int64_t launches;
+    int64_t bfs_launches;
+    double bfs_ms;
+    int64_t bfs_levels;
+    int64_t bfs_batches;
+} hm_stats;
+hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_H */

@@ -1,0 +1,331 @@
+// Psi for one graph (PAPER.md:121-122 §3; :209 §4): all-sources BFS closeness.
+//
+// Pipeline (all device-side, stream-ordered, no host synchronisation):
+//   1. connected components (lock-free union-find, hooks larger root under
+//      smaller, so the label is the smallest vertex id of the component);
+//   2. relabel: components sorted by (size desc, smallest id asc), vertices by
+//      (component rank, id); isolated vertices last and excluded from the BFS;
+//   3. relabelled CSR + per-row component info + heavy-row list;
+//   4. persistent MS-BFS (msbfs.cu) -> S per relabelled row;
+//   5. finalize in original order: S, k, Wasserman-Faust closeness, n-penalty
+//      sum, degree;
+//   6. mu = RN(exact sum c) / V (exactsum.cu) and CH = {v : c(v) > mu}.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "msbfs.cuh"
+
+namespace hm {
+namespace {
+
+constexpr int TB = 256;
+
+__device__ __forceinline__ int cc_find(int32_t *p, int x) {
+    while (true) {
+        const int px = __ldcg(p + x);
+        if (px == x) return x;
+        const int ppx = __ldcg(p + px);
+        if (ppx != px) p[x] = ppx;     // path halving: ppx is an ancestor of x
+        x = px;
+    }
+}
+
+__global__ void k_iota(int32_t *p, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+// warp per row u; unite(u, v) for arcs with v > u
+__global__ void k_cc_union(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           int32_t *p, int V) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = w0; u < V; u += nw) {
+        const int rb = row_ptr[u], re = row_ptr[u + 1];
+        for (int j = rb + lane; j < re; j += 32) {
+            const int v = col[j];
+            if (v <= u) continue;
+            int ru = cc_find(p, (int)u), rv = cc_find(p, v);
+            while (ru != rv) {
+                if (ru < rv) { const int t = ru; ru = rv; rv = t; }   // ru > rv: hook ru under rv
+                const int old = atomicCAS(p + ru, ru, rv);
+                if (old == ru) break;
+                ru = cc_find(p, old);
+                rv = cc_find(p, rv);
+            }
+        }
+    }
+}
+
+__global__ void k_cc_compress(int32_t *p, int32_t *csize, int V) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const int r = cc_find(p, v);
+        p[v] = r;
+        atomicAdd(csize + r, 1);
+    }
+}
+
+// component keys: roots -> ((V - size) << 32 | root); others -> V << 32 (sort last)
+__global__ void k_comp_keys(const int32_t *label, const int32_t *csize, uint64_t *key, int V) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+        key[v] = (label[v] == v) ? (((uint64_t)(V - csize[v]) << 32) | (uint32_t)v)
+                                 : ((uint64_t)V << 32);
+}
+
+// sorted component table; scalars[1] = n_giant (if > 1), scalars[2] = n_comp
+__global__ void k_comp_tables(const uint64_t *keys, int32_t *size_s, int32_t *rank_of_root,
+                              int32_t *scalars, int V) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const bool valid = (k >> 32) < (uint64_t)V;
+        if (valid) {
+            const int sz = V - (int)(k >> 32);
+            const int root = (int)(k & 0xffffffffull);
+            size_s[i] = sz;
+            rank_of_root[root] = i;
+            if (i == 0) scalars[1] = sz > 1 ? sz : 0;
+            const bool last = (i + 1 == V) || ((keys[i + 1] >> 32) >= (uint64_t)V);
+            if (last) scalars[2] = i + 1;
+        } else {
+            size_s[i] = 0;
+        }
+    }
+}
+
+// scalars[0] = n_live = first row of the first singleton component
+__global__ void k_nlive(const int32_t *size_s, const int32_t *cstart, int32_t *scalars, int V) {
+    const int n_comp = scalars[2];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_comp; i += gridDim.x * blockDim.x)
+        if (size_s[i] > 1 && (i + 1 == n_comp || size_s[i + 1] <= 1)) scalars[0] = cstart[i] + size_s[i];
+}
+
+__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, uint64_t *key, int V) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+        key[v] = ((uint64_t)rank_of_root[label[v]] << 32) | (uint32_t)v;
+}
+
+__global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32_t *size_s,
+                       const int32_t *cstart, int32_t *new_to_old, int32_t *old_to_new,
+                       int32_t *new_deg, int2 *cinfo, int V) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const int old = (int)(k & 0xffffffffull);
+        const int r = (int)(k >> 32);
+        new_to_old[i] = old;
+        old_to_new[old] = i;
+        new_deg[i] = row_ptr[old + 1] - row_ptr[old];
+        cinfo[i] = make_int2(cstart[r], size_s[r]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) new_deg[V] = 0;
+}
+
+__global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                               const int32_t *__restrict__ nrp, const int32_t *__restrict__ new_to_old,
+                               const int32_t *__restrict__ old_to_new, int32_t *__restrict__ ncol,
+                               int32_t *heavy, int32_t *scalars, int heavy_deg, int V) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int n_live = scalars[0];
+    for (int64_t i = w0; i < n_live; i += nw) {
+        const int old = new_to_old[i];
+        const int rb = row_ptr[old], re = row_ptr[old + 1];
+        const int ob = nrp[i];
+        for (int j = rb + lane; j < re; j += 32) ncol[ob + (j - rb)] = old_to_new[col[j]];
+        if (lane == 0 && re - rb > heavy_deg) heavy[atomicAdd(scalars + 3, 1)] = (int)i;
+    }
+}
+
+__global__ void k_finalize(const int32_t *old_to_new, const int32_t *label, const int32_t *csize,
+                           const int32_t *row_ptr, const uint64_t *S_rel, const int32_t *scalars,
+                           uint64_t *S, int32_t *kk, double *c, uint64_t *pen, int32_t *deg, int V) {
+    const int n_live = scalars[0];
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const int i = old_to_new[v];
+        const uint64_t s = (i < n_live) ? S_rel[i] : 0ull;
+        const int k = csize[label[v]];
+        // Wasserman-Faust closeness exactly as NetworkX evaluates it:
+        // ((k-1)/S) * ((k-1)/(V-1)), binary64 RN, 0 if S == 0 or V <= 1.
+        double cv = 0.0;
+        if (s > 0ull && V > 1) {
+            const double t1 = __ddiv_rn((double)(k - 1), (double)s);
+            const double t2 = __ddiv_rn((double)(k - 1), (double)(V - 1));
+            cv = __dmul_rn(t1, t2);
+        }
+        S[v] = s;
+        kk[v] = k;
+        c[v] = cv;
+        pen[v] = s + (uint64_t)(V - k) * (uint64_t)V;   // n-penalty sum
+        deg[v] = row_ptr[v + 1] - row_ptr[v];
+    }
+}
+
+// CH bitmap: bit v set iff c[v] > mu (strict); popcount into *count
+__global__ void k_cc_bitmap(const double *c, const double *mu, uint32_t *bm, int32_t *count, int V) {
+    const int lane = threadIdx.x & 31;
+    const double m = *mu;
+    for (int64_t vb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31LL; vb < V;
+         vb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vb + lane;
+        const bool in = v < V && c[v] > m;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) {
+            bm[vb >> 5] = b;
+            if (b) atomicAdd(count, __popc(b));
+        }
+    }
+}
+
+inline int nbits(uint64_t x) {
+    int b = 0;
+    while (x) { ++b; x >>= 1; }
+    return b;
+}
+
+}  // namespace
+
+void closeness(hm_ctx *ctx, Graph &G) {
+    cudaStream_t s = ctx->stream;
+    const int V = G.V;
+    const int W = ctx->params.bfs_words;
+    const unsigned gb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
+    const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
+    const int end_bit = 32 + nbits((uint64_t)V);
+
+    // per-graph outputs
+    if (!G.S.p || G.S.bytes < (size_t)V * 8) {
+        G.S.alloc((size_t)V * 8, s);
+        G.k.alloc((size_t)V * 4, s);
+        G.c.alloc((size_t)V * 8, s);
+        G.pen.alloc((size_t)V * 8, s);
+        G.deg.alloc((size_t)V * 4, s);
+        G.ch.alloc((size_t)((V + 31) / 32) * 4 + 8 + 8, s);   // bitmap + mu + count
+    }
+
+    Buf label((size_t)V * 4, s), csize((size_t)V * 4, s);
+    Buf key1((size_t)V * 8, s), key2((size_t)V * 8, s);
+    Buf size_s((size_t)V * 4, s), cstart((size_t)V * 4, s), rank((size_t)V * 4, s);
+    Buf n2o((size_t)V * 4, s), o2n((size_t)V * 4, s), ndeg((size_t)(V + 1) * 4, s);
+    Buf nrp((size_t)(V + 1) * 4, s), cinfo((size_t)V * 8, s);
+    Buf ncol((size_t)(G.nnz > 0 ? G.nnz : 1) * 4, s), heavy((size_t)V * 4, s);
+    Buf scal(64, s);
+    int32_t *scalars = scal.as<int32_t>();
+    HM_CUDA(cudaMemsetAsync(scal.p, 0, 64, s));
+    HM_CUDA(cudaMemsetAsync(csize.p, 0, csize.bytes, s));
+
+    // 1. connected components
+    k_iota<<<gb, TB, 0, s>>>(label.as<int32_t>(), V);
+    k_cc_union<<<gw, TB, 0, s>>>(G.row_ptr.as<int32_t>(), G.col.as<int32_t>(), label.as<int32_t>(), V);
+    k_cc_compress<<<gb, TB, 0, s>>>(label.as<int32_t>(), csize.as<int32_t>(), V);
+    check_launch("cc");
+    count_launch(ctx, 3);
+
+    // 2. component order and vertex order
+    k_comp_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), csize.as<int32_t>(), key1.as<uint64_t>(), V);
+    count_launch(ctx);
+    {
+        size_t tb = 0;
+        HM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
+                                               end_bit, s));
+        size_t tb2 = 0;
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, size_s.as<int32_t>(), cstart.as<int32_t>(), V + 1, s));
+        if (tb2 > tb) tb = tb2;
+        Buf tmp(tb, s);
+        HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
+                                               end_bit, s));
+        k_comp_tables<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), size_s.as<int32_t>(), rank.as<int32_t>(),
+                                       scalars, V);
+        size_t tbs = tb;
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, size_s.as<int32_t>(), cstart.as<int32_t>(), V, s));
+        k_nlive<<<gb, TB, 0, s>>>(size_s.as<int32_t>(), cstart.as<int32_t>(), scalars, V);
+        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), key1.as<uint64_t>(), V);
+        tbs = tb;
+        HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tbs, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
+                                               end_bit, s));
+        k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), G.row_ptr.as<int32_t>(), size_s.as<int32_t>(),
+                                cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
+                                ndeg.as<int32_t>(), cinfo.as<int2>(), V);
+        tbs = tb;
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, ndeg.as<int32_t>(), nrp.as<int32_t>(), V + 1, s));
+        check_launch("relabel");
+        count_launch(ctx, 4 + 3 * 4 + 2);   // our kernels + CUB passes (approximate)
+    }
+    // 3. relabelled CSR + heavy list
+    k_relabel_cols<<<gw, TB, 0, s>>>(G.row_ptr.as<int32_t>(), G.col.as<int32_t>(), nrp.as<int32_t>(),
+                                     n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
+                                     heavy.as<int32_t>(), scalars, ctx->params.bfs_heavy, V);
+    check_launch("k_relabel_cols");
+    count_launch(ctx);
+
+    // 4. MS-BFS
+    const size_t rowb = (size_t)W * 8;
+    const size_t bmw = (size_t)(V + 31) / 32 + 1;
+    Buf vis((size_t)V * rowb, s), F0((size_t)V * rowb, s), F1((size_t)V * rowb, s);
+    Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), flags(16, s);
+    HM_CUDA(cudaMemsetAsync(Srel.p, 0, Srel.bytes, s));
+    HM_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, s));
+    BfsArgs a;
+    a.row_ptr = nrp.as<int32_t>();
+    a.col = ncol.as<int32_t>();
+    a.cinfo = cinfo.as<int2>();
+    a.comp_size = size_s.as<int32_t>();
+    a.comp_start = cstart.as<int32_t>();
+    a.scalars = scalars;
+    a.heavy = heavy.as<int32_t>();
+    a.heavy_deg = ctx->params.bfs_heavy;
+    a.vis = vis.as<uint64_t>();
+    a.F0 = F0.as<uint64_t>();
+    a.F1 = F1.as<uint64_t>();
+    uint32_t *bm = bms.as<uint32_t>();
+    a.chg0 = bm;
+    a.chg1 = bm + bmw;
+    a.chg2 = bm + 2 * bmw;
+    a.done = bm + 3 * bmw;
+    a.touched = bm + 4 * bmw;
+    a.S = Srel.as<uint64_t>();
+    a.flags = flags.as<int32_t>();
+    a.counters = ctx->dstats.as<unsigned long long>();
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->params.timing) {
+        HM_CUDA(cudaEventCreate(&e0));
+        HM_CUDA(cudaEventCreate(&e1));
+        HM_CUDA(cudaEventRecord(e0, s));
+    }
+    const int grid = launch_msbfs(W, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
+    if (grid < 0) {
+        cudaGetLastError();
+        throw Error(HM_ECUDA, "msbfs launch failed (" + std::to_string(grid) + ")");
+    }
+    check_launch("msbfs");
+    if (ctx->params.timing) {
+        HM_CUDA(cudaEventRecord(e1, s));
+        ctx->pending.push_back({e0, e1});   // resolved in hm_get_stats (no sync here)
+    }
+    count_launch(ctx);
+    ctx->stats.bfs_launches += 1;
+
+    // 5. finalize
+    k_finalize<<<gb, TB, 0, s>>>(o2n.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(),
+                                 G.row_ptr.as<int32_t>(), Srel.as<uint64_t>(), scalars, G.S.as<uint64_t>(),
+                                 G.k.as<int32_t>(), G.c.as<double>(), G.pen.as<uint64_t>(),
+                                 G.deg.as<int32_t>(), V);
+    check_launch("k_finalize");
+    count_launch(ctx);
+
+    // 6. mean closeness (exact) and CC nodes
+    uint32_t *chbm = G.ch.as<uint32_t>();
+    const size_t nbw = (size_t)(V + 31) / 32;
+    double *d_mu = reinterpret_cast<double *>(reinterpret_cast<char *>(chbm) + ((nbw * 4 + 7) / 8) * 8);
+    int32_t *d_cnt = reinterpret_cast<int32_t *>(d_mu + 1);
+    exact_mean(ctx, G.c.as<double>(), V, nullptr, d_mu, nullptr);
+    HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
+    k_cc_bitmap<<<grid_for((int64_t)V, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(G.c.as<double>(), d_mu, chbm,
+                                                                                   d_cnt, V);
+    check_launch("k_cc_bitmap");
+    count_launch(ctx);
+    G.has_results = true;
+}
+
+}  // namespace hm

@@ -1,0 +1,151 @@
+// Shared internals of libhm (B200 / sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <utility>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/hm.h"
+
+namespace hm {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    hm_status code;
+    Error(hm_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define HM_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t _e = (call);                                                       \
+        if (_e != cudaSuccess)                                                         \
+            throw ::hm::Error(_e == cudaErrorMemoryAllocation ? HM_ENOMEM : HM_ECUDA,  \
+                              std::string(#call) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+
+#define HM_REQUIRE(cond, code, msg)                 \
+    do {                                            \
+        if (!(cond)) throw ::hm::Error(code, msg);  \
+    } while (0)
+
+// ------------------------------------------------------- device buffers
+// Stream-ordered allocation (cudaMallocAsync) owned by RAII handles.
+struct Buf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    Buf() = default;
+    Buf(size_t n, cudaStream_t st) { alloc(n, st); }
+    Buf(const Buf &) = delete;
+    Buf &operator=(const Buf &) = delete;
+    Buf(Buf &&o) noexcept { *this = std::move(o); }
+    Buf &operator=(Buf &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; bytes = o.bytes; s = o.s;
+            o.p = nullptr; o.bytes = 0;
+        }
+        return *this;
+    }
+    ~Buf() { release(); }
+    void alloc(size_t n, cudaStream_t st) {
+        release();
+        s = st;
+        bytes = n;
+        if (n) HM_CUDA(cudaMallocAsync(&p, n, st));
+    }
+    // grow-only scratch
+    void ensure(size_t n, cudaStream_t st) {
+        if (n > bytes || p == nullptr) alloc(n < 64 ? 64 : n, st);
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// ------------------------------------------------------- per-graph state
+struct Graph {
+    bool alive = false;
+    bool is_layer = false;
+    int32_t V = 0;
+    int64_t nnz = 0;          // arcs = 2 m
+    Buf row_ptr, col;         // CSR, rows ascending
+    // cached Psi results (valid when has_results)
+    bool has_results = false;
+    Buf S, k, c, pen, deg, ch;   // uint64, int32, double, uint64, int32, uint32 bitmap
+    double mu = 0.0;
+    int32_t ch_count = 0;
+};
+
+struct Params {
+    int bfs_words = 16;
+    int bfs_heavy = 256;
+    int bfs_blocks_per_sm = 0;
+    int timing = 0;
+};
+
+struct Stats {
+    int64_t launches = 0;
+    int64_t bfs_launches = 0;
+    double bfs_ms = 0;
+};
+
+}  // namespace hm
+
+struct hm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    std::vector<hm::Graph> graphs;
+    int32_t n_layers = 0;
+    hm::Params params;
+    hm::Stats stats;
+    hm::Buf dstats;           // device counters: [0] levels, [1] batches (uint64)
+    int num_sms = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;   // MS-BFS launch events (timing=1)
+};
+
+namespace hm {
+
+inline void count_launch(hm_ctx *ctx, int n = 1) { ctx->stats.launches += n; }
+
+inline void check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(HM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148LL * 32) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (unsigned)b;
+}
+
+Graph &graph(hm_ctx *ctx, int32_t g);                 // throws ESTATE
+bool is_device_ptr(const void *p);
+void copy_out(hm_ctx *ctx, void *dst, const void *dsrc, size_t bytes);  // host or device dst
+
+// module entry points (each file)
+void build_csr(hm_ctx *ctx, int32_t V, const int32_t *edges_host_or_dev, int64_t m, Graph &G,
+               int64_t *dropped);
+void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, Graph &out);
+void closeness(hm_ctx *ctx, Graph &G);
+// exact (correctly rounded) sum of masked non-negative doubles, then mean = sum / count;
+// result written to device double *d_mean (count taken from mask popcount or n)
+void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask_or_null,
+                double *d_mean_out, int32_t *d_count_out);
+void degrees(hm_ctx *ctx, const Graph &G, int32_t *d_deg);
+// keys ordering closeness descending: ~bits(c) (c >= 0, so bit patterns are monotone)
+void closeness_desc_keys(hm_ctx *ctx, const double *d_c, int32_t V, uint64_t *d_keys);
+void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_ids_out);
+void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t K,
+             int32_t *ids_out, int32_t *count_out);
+
+}  // namespace hm

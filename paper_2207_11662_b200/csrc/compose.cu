@@ -1,0 +1,215 @@
+// Composition Theta (§5): CC2 (Alg. 1), CC1 (Eq. 2, Eq. 3 and
+// its pseudocode) and the naive baseline, over r >= 2 layers' cached Psi
+// results.  Only per-layer results and the layers' own neighbourhoods (NBD,
+// PAPER.md:431) are read -- never an AND aggregate.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hm {
+namespace {
+
+constexpr int TB = 256;
+constexpr int RMAX = 8;
+
+struct LayerPtrs {
+    const uint64_t *pen[RMAX];
+    const int32_t *deg[RMAX];
+    const uint32_t *ch[RMAX];
+    const int32_t *rp[RMAX];
+    const int32_t *cl[RMAX];
+    int r;
+};
+
+// CC2 (Alg. 1): estSumDist(u) = max_i sumDist_i(u) (n-penalty
+// sums, reading Z3).  Ranking by Eq. 1 (n-1)/est descending == est ascending.
+__global__ void k_cc2_keys(LayerPtrs L, int V, uint64_t *key) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        uint64_t e = L.pen[0][v];
+        for (int i = 1; i < L.r; ++i) e = max(e, L.pen[i][v]);
+        key[v] = e;
+    }
+}
+
+// naive: common CC nodes; key 0 for members (ranked by id), ~0 otherwise
+__global__ void k_naive_keys(LayerPtrs L, int V, uint64_t *key, int32_t *count) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t vb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31LL; vb < V;
+         vb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vb + lane;
+        uint32_t w = 0xffffffffu;
+        for (int i = 0; i < L.r; ++i) w &= L.ch[i][vb >> 5];
+        if (vb + 32 > V) w &= (V - vb >= 32) ? 0xffffffffu : ((1u << (V - vb)) - 1u);
+        if (v < V) key[v] = ((w >> lane) & 1u) ? 0ull : ~0ull;
+        if (lane == 0 && w) atomicAdd(count, __popc(w));
+    }
+}
+
+// CC1 step 1 (Eq. 2): mindeg, ratio_i = pen_i / mindeg (+inf if mindeg = 0, Z8),
+// finite mask F
+__global__ void k_cc1_ratios(LayerPtrs L, int V, int32_t *mindeg, double *ratio, uint8_t *fin) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        int md = L.deg[0][v];
+        for (int i = 1; i < L.r; ++i) md = min(md, L.deg[i][v]);
+        mindeg[v] = md;
+        fin[v] = md >= 1;
+        for (int i = 0; i < L.r; ++i)
+            ratio[(size_t)i * V + v] = md >= 1 ? __ddiv_rn((double)L.pen[i][v], (double)md) : (double)INFINITY;
+    }
+}
+
+// Eq. 3: avgAND = max_i avg_i  (avg_i = 0 if no finite ratio)
+__global__ void k_cc1_avgand(const double *avgs, int r, double *avg_and) {
+    if (threadIdx.x != 0) return;
+    double m = avgs[0];
+    for (int i = 1; i < r; ++i) m = fmax(m, avgs[i]);
+    *avg_and = m;
+}
+
+__device__ __forceinline__ bool bsearch_row(const int32_t *__restrict__ col, int lo, int hi, int v) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int x = col[mid];
+        if (x == v) return true;
+        if (x < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return false;
+}
+
+// CC1 main loop (pseudocode PAPER.md:486-507, flat r-ary, Z7-Z12): warp per
+// common CC node u.  I = ∩_i {v ∈ NBD_i(u) : ratio_i(v) < avgAND}; if |I| > 1
+// add I; always add u.  R is a bitmap (atomicOr -- set union is order-free).
+__global__ void k_cc1_main(LayerPtrs L, int V, const double *ratio, const double *avg_and_p, uint32_t *R) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double avg_and = *avg_and_p;
+    for (int64_t u = w0; u < V; u += nw) {
+        bool common = true;
+        for (int i = 0; i < L.r; ++i) common = common && ((L.ch[i][u >> 5] >> (u & 31)) & 1u);
+        if (!common) continue;
+        // driver: the layer with the shortest row u
+        int drv = 0, best = 0x7fffffff;
+        for (int i = 0; i < L.r; ++i) {
+            const int d = L.rp[i][u + 1] - L.rp[i][u];
+            if (d < best) { best = d; drv = i; }
+        }
+        const int rb = L.rp[drv][u], re = L.rp[drv][u + 1];
+        int cnt = 0;
+        // pass 1: count |I|
+        for (int j = rb + lane; j < re; j += 32) {
+            const int v = L.cl[drv][j];
+            bool in = true;
+            for (int i = 0; i < L.r && in; ++i) {
+                in = ratio[(size_t)i * V + v] < avg_and;
+                if (in && i != drv) in = bsearch_row(L.cl[i], L.rp[i][u], L.rp[i][u + 1], v);
+            }
+            cnt += in ? 1 : 0;
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (cnt > 1) {
+            for (int j = rb + lane; j < re; j += 32) {
+                const int v = L.cl[drv][j];
+                bool in = true;
+                for (int i = 0; i < L.r && in; ++i) {
+                    in = ratio[(size_t)i * V + v] < avg_and;
+                    if (in && i != drv) in = bsearch_row(L.cl[i], L.rp[i][u], L.rp[i][u + 1], v);
+                }
+                if (in) atomicOr(&R[v >> 5], 1u << (v & 31));
+            }
+        }
+        if (lane == 0) atomicOr(&R[u >> 5], 1u << (u & 31));
+    }
+}
+
+// CC1 ranking (Z13): members keyed by the bits of RN(est/mindeg) (positive
+// doubles order as their bit patterns), others ~0; |R| into *count.
+__global__ void k_cc1_keys(LayerPtrs L, int V, const uint32_t *R, const int32_t *mindeg, uint64_t *key,
+                           int32_t *count) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t vb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31LL; vb < V;
+         vb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vb + lane;
+        const uint32_t w = R[vb >> 5];
+        if (v < V) {
+            if ((w >> lane) & 1u) {
+                uint64_t e = L.pen[0][v];
+                for (int i = 1; i < L.r; ++i) e = max(e, L.pen[i][v]);
+                const double q = __ddiv_rn((double)e, (double)mindeg[v]);
+                key[v] = (uint64_t)__double_as_longlong(q);
+            } else {
+                key[v] = ~0ull;
+            }
+        }
+        if (lane == 0 && w) atomicAdd(count, __popc(w));
+    }
+}
+
+}  // namespace
+
+void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t K, int32_t *ids_out,
+             int32_t *count_out) {
+    cudaStream_t s = ctx->stream;
+    const int r = (int)gs.size();
+    HM_REQUIRE(r >= 2 && r <= RMAX, HM_EINVAL, "compose needs 2 <= r <= 8 layers");
+    const int V = gs[0]->V;
+    HM_REQUIRE(K >= 1 && K <= V, HM_EINVAL, "K must be in [1, V]");
+    LayerPtrs L;
+    L.r = r;
+    for (int i = 0; i < r; ++i) {
+        HM_REQUIRE(gs[i]->has_results, HM_ESTATE, "compose before hm_closeness on an input graph");
+        HM_REQUIRE(gs[i]->V == V, HM_EINVAL, "graphs differ in V");
+        L.pen[i] = gs[i]->pen.as<uint64_t>();
+        L.deg[i] = gs[i]->deg.as<int32_t>();
+        L.ch[i] = gs[i]->ch.as<uint32_t>();
+        L.rp[i] = gs[i]->row_ptr.as<int32_t>();
+        L.cl[i] = gs[i]->col.as<int32_t>();
+    }
+    const unsigned g = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
+    const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
+    Buf keys((size_t)V * 8, s), ids((size_t)K * 4, s), cnt(8, s);
+    HM_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+    int32_t Kout = K;
+    if (heuristic == HM_CC2) {
+        k_cc2_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>());
+        check_launch("k_cc2_keys");
+        count_launch(ctx);
+        topk(ctx, keys.as<uint64_t>(), V, K, ids.as<int32_t>());
+        if (count_out) *count_out = K;
+    } else if (heuristic == HM_NAIVE || heuristic == HM_CC1) {
+        if (heuristic == HM_NAIVE) {
+            k_naive_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>(), cnt.as<int32_t>());
+            check_launch("k_naive_keys");
+            count_launch(ctx);
+        } else {
+            Buf mindeg((size_t)V * 4, s), ratio((size_t)V * r * 8, s), fin((size_t)V, s);
+            Buf avgs((size_t)(r + 1) * 8, s), R((size_t)((V + 31) / 32) * 4, s);
+            HM_CUDA(cudaMemsetAsync(R.p, 0, R.bytes, s));
+            k_cc1_ratios<<<g, TB, 0, s>>>(L, V, mindeg.as<int32_t>(), ratio.as<double>(), fin.as<uint8_t>());
+            count_launch(ctx);
+            for (int i = 0; i < r; ++i)
+                exact_mean(ctx, ratio.as<double>() + (size_t)i * V, V, fin.as<uint8_t>(), avgs.as<double>() + i,
+                           nullptr);
+            k_cc1_avgand<<<1, 32, 0, s>>>(avgs.as<double>(), r, avgs.as<double>() + r);
+            k_cc1_main<<<gw, TB, 0, s>>>(L, V, ratio.as<double>(), avgs.as<double>() + r, R.as<uint32_t>());
+            k_cc1_keys<<<g, TB, 0, s>>>(L, V, R.as<uint32_t>(), mindeg.as<int32_t>(), keys.as<uint64_t>(),
+                                       cnt.as<int32_t>());
+            check_launch("cc1");
+            count_launch(ctx, 3);
+        }
+        int32_t nR = 0;
+        HM_CUDA(cudaMemcpyAsync(&nR, cnt.p, 4, cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        Kout = nR < K ? nR : K;
+        if (Kout > 0) topk(ctx, keys.as<uint64_t>(), V, Kout, ids.as<int32_t>());
+        if (count_out) *count_out = nR;
+    } else {
+        throw Error(HM_EINVAL, "unknown heuristic");
+    }
+    if (Kout > 0) copy_out(ctx, ids_out, ids.p, (size_t)Kout * 4);
+}
+
+}  // namespace hm

@@ -1,0 +1,323 @@
+// C ABI entry points (include/hm.h).  Argument checking, graph registry,
+// host/device output handling; every computation is delegated to the kernels
+// in graph.cu, closeness.cu, msbfs.cu, exactsum.cu, topk.cu and compose.cu.
+#include <cuda_runtime.h>
+#include <string.h>
+#include <algorithm>
+#include <set>
+
+#include "common.cuh"
+
+namespace hm {
+
+Graph &graph(hm_ctx *ctx, int32_t g) {
+    HM_REQUIRE(g >= 0 && g < (int32_t)ctx->graphs.size() && ctx->graphs[g].alive, HM_ESTATE,
+               "unknown or freed graph id " + std::to_string(g));
+    return ctx->graphs[g];
+}
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+void copy_out(hm_ctx *ctx, void *dst, const void *dsrc, size_t bytes) {
+    if (!dst || !bytes) return;
+    if (is_device_ptr(dst)) {
+        HM_CUDA(cudaMemcpyAsync(dst, dsrc, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+        HM_CUDA(cudaMemcpyAsync(dst, dsrc, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+}
+
+}  // namespace hm
+
+using namespace hm;
+
+#define HM_API_BEGIN(ctx)                                   \
+    if (!(ctx)) return HM_EINVAL;                           \
+    try {                                                   \
+        HM_CUDA(cudaSetDevice((ctx)->device));
+#define HM_API_END(ctx)                                     \
+        (ctx)->err.clear();                                 \
+        return HM_OK;                                       \
+    } catch (const hm::Error &e) {                          \
+        (ctx)->err = e.what();                              \
+        return e.code;                                      \
+    } catch (const std::exception &e) {                    \
+        (ctx)->err = e.what();                              \
+        return HM_ECUDA;                                    \
+    }
+
+extern "C" {
+
+hm_status hm_create(hm_ctx **out, int device, void *cuda_stream) {
+    if (!out) return HM_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return HM_ECUDA;
+    }
+    hm_ctx *ctx = new hm_ctx();
+    ctx->device = device;
+    try {
+        HM_CUDA(cudaSetDevice(device));
+        if (cuda_stream) {
+            ctx->stream = (cudaStream_t)cuda_stream;
+        } else {
+            HM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+        HM_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+        int coop = 0;
+        HM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+        HM_REQUIRE(coop, HM_ECUDA, "device lacks cooperative launch");
+        // keep freed stream-ordered memory in the pool (no release at sync points)
+        cudaMemPool_t pool;
+        HM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        HM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        HM_CUDA(cudaEventCreate(&ctx->ev0));
+        HM_CUDA(cudaEventCreate(&ctx->ev1));
+        ctx->dstats.alloc(64, ctx->stream);
+        HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));
+        HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (const hm::Error &) {
+        hm_destroy(ctx);
+        return HM_ECUDA;
+    }
+    *out = ctx;
+    return HM_OK;
+}
+
+void hm_destroy(hm_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    ctx->graphs.clear();
+    ctx->dstats.release();
+    for (auto &pe : ctx->pending) {
+        cudaEventDestroy(pe.first);
+        cudaEventDestroy(pe.second);
+    }
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *hm_last_error(const hm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(name, HM_EINVAL, "null name");
+    const std::string n(name);
+    if (n == "bfs_words") {
+        HM_REQUIRE(value == 8 || value == 16 || value == 32, HM_EINVAL, "bfs_words must be 8, 16 or 32");
+        ctx->params.bfs_words = (int)value;
+    } else if (n == "bfs_heavy") {
+        HM_REQUIRE(value >= 1, HM_EINVAL, "bfs_heavy must be >= 1");
+        ctx->params.bfs_heavy = (int)value;
+    } else if (n == "bfs_blocks_per_sm") {
+        HM_REQUIRE(value >= 0, HM_EINVAL, "bfs_blocks_per_sm must be >= 0");
+        ctx->params.bfs_blocks_per_sm = (int)value;
+    } else if (n == "timing") {
+        ctx->params.timing = value ? 1 : 0;
+    } else {
+        throw Error(HM_EINVAL, "unknown parameter " + n);
+    }
+    HM_API_END(ctx)
+}
+
+hm_status hm_load_layers(hm_ctx *ctx, int32_t V, int32_t l, const int32_t *const *edges, const int64_t *m,
+                         int64_t *dropped_out) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(V > 0 && l >= 1, HM_EINVAL, "need V > 0 and l >= 1");
+    HM_REQUIRE(edges && m, HM_EINVAL, "null edges / m");
+    for (int i = 0; i < l; ++i) {
+        HM_REQUIRE(m[i] >= 0, HM_EINVAL, "negative edge count");
+        HM_REQUIRE(m[i] == 0 || edges[i], HM_EINVAL, "null edge array");
+        HM_REQUIRE(2 * m[i] < (int64_t)INT32_MAX, HM_ERANGE, "2*m >= 2^31 arcs does not fit an int32 CSR");
+    }
+    std::vector<Graph> gs(l);
+    std::vector<int64_t> dropped(l, 0);
+    for (int i = 0; i < l; ++i) {
+        build_csr(ctx, V, edges[i], m[i], gs[i], &dropped[i]);
+        gs[i].alive = true;
+        gs[i].is_layer = true;
+    }
+    HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->graphs = std::move(gs);
+    ctx->n_layers = l;
+    if (dropped_out)
+        for (int i = 0; i < l; ++i) dropped_out[i] = dropped[i];
+    HM_API_END(ctx)
+}
+
+hm_status hm_graph_info(hm_ctx *ctx, int32_t g, int32_t *V, int64_t *m_undirected, const int32_t **d_row_ptr,
+                        const int32_t **d_col) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    if (V) *V = G.V;
+    if (m_undirected) *m_undirected = G.nnz / 2;
+    if (d_row_ptr) *d_row_ptr = G.row_ptr.as<int32_t>();
+    if (d_col) *d_col = G.col.as<int32_t>();
+    HM_API_END(ctx)
+}
+
+hm_status hm_graph_csr(hm_ctx *ctx, int32_t g, int32_t *row_ptr, int32_t *col) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    copy_out(ctx, row_ptr, G.row_ptr.p, (size_t)(G.V + 1) * 4);
+    copy_out(ctx, col, G.col.p, (size_t)G.nnz * 4);
+    HM_API_END(ctx)
+}
+
+static hm_status aggregate(hm_ctx *ctx, const int32_t *ids, int32_t r, int32_t *g_out, bool is_and) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(ids && g_out, HM_EINVAL, "null argument");
+    HM_REQUIRE(r >= 2, HM_EINVAL, "aggregation needs r >= 2");
+    HM_REQUIRE(r <= 8, HM_EINVAL, "aggregation supports r <= 8");
+    std::set<int32_t> seen(ids, ids + r);
+    HM_REQUIRE((int32_t)seen.size() == r, HM_EINVAL, "repeated graph id");
+    std::vector<Graph *> in;
+    for (int i = 0; i < r; ++i) in.push_back(&graph(ctx, ids[i]));
+    for (int i = 1; i < r; ++i) HM_REQUIRE(in[i]->V == in[0]->V, HM_EINVAL, "graphs differ in V");
+    Graph out;
+    and_or_aggregate(ctx, in, is_and, out);
+    // reuse a freed slot, else append (pointers in `in` are not used after this)
+    int32_t slot = -1;
+    for (int32_t i = ctx->n_layers; i < (int32_t)ctx->graphs.size(); ++i)
+        if (!ctx->graphs[i].alive) { slot = i; break; }
+    if (slot < 0) {
+        ctx->graphs.emplace_back();
+        slot = (int32_t)ctx->graphs.size() - 1;
+    }
+    ctx->graphs[slot] = std::move(out);
+    *g_out = slot;
+    HM_API_END(ctx)
+}
+
+hm_status hm_and_aggregate(hm_ctx *ctx, const int32_t *graph_ids, int32_t r, int32_t *g_out) {
+    return aggregate(ctx, graph_ids, r, g_out, true);
+}
+
+hm_status hm_or_aggregate(hm_ctx *ctx, const int32_t *graph_ids, int32_t r, int32_t *g_out) {
+    return aggregate(ctx, graph_ids, r, g_out, false);
+}
+
+hm_status hm_free_graph(hm_ctx *ctx, int32_t g) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    HM_REQUIRE(!G.is_layer, HM_ESTATE, "layers cannot be freed individually");
+    G = Graph();
+    HM_API_END(ctx)
+}
+
+hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach, double *closeness_out,
+                       uint64_t *pen_sum) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    closeness(ctx, G);
+    const size_t V = (size_t)G.V;
+    copy_out(ctx, dist_sum, G.S.p, V * 8);
+    copy_out(ctx, reach, G.k.p, V * 4);
+    copy_out(ctx, closeness_out, G.c.p, V * 8);
+    copy_out(ctx, pen_sum, G.pen.p, V * 8);
+    HM_API_END(ctx)
+}
+
+hm_status hm_cc_nodes(hm_ctx *ctx, int32_t g, uint32_t *bitmap, int32_t *count, double *mean) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    HM_REQUIRE(G.has_results, HM_ESTATE, "hm_cc_nodes before hm_closeness");
+    const size_t nbw = (size_t)(G.V + 31) / 32;
+    copy_out(ctx, bitmap, G.ch.p, nbw * 4);
+    const char *base = G.ch.as<char>() + ((nbw * 4 + 7) / 8) * 8;
+    struct { double mu; int32_t cnt; int32_t pad; } h;
+    HM_CUDA(cudaMemcpyAsync(&h, base, 12, cudaMemcpyDeviceToHost, ctx->stream));
+    HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (count) *count = h.cnt;
+    if (mean) *mean = h.mu;
+    HM_API_END(ctx)
+}
+
+hm_status hm_degrees(hm_ctx *ctx, int32_t g, int32_t *deg) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    HM_REQUIRE(deg, HM_EINVAL, "null deg");
+    Buf tmp((size_t)G.V * 4, ctx->stream);
+    degrees(ctx, G, tmp.as<int32_t>());
+    copy_out(ctx, deg, tmp.p, (size_t)G.V * 4);
+    HM_API_END(ctx)
+}
+
+hm_status hm_topk_closeness(hm_ctx *ctx, int32_t g, int32_t K, int32_t *ids_out) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    HM_REQUIRE(G.has_results, HM_ESTATE, "hm_topk_closeness before hm_closeness");
+    HM_REQUIRE(K >= 1 && K <= G.V, HM_EINVAL, "K must be in [1, V]");
+    HM_REQUIRE(ids_out, HM_EINVAL, "null ids_out");
+    Buf keys((size_t)G.V * 8, ctx->stream), ids((size_t)K * 4, ctx->stream);
+    closeness_desc_keys(ctx, G.c.as<double>(), G.V, keys.as<uint64_t>());
+    topk(ctx, keys.as<uint64_t>(), G.V, K, ids.as<int32_t>());
+    copy_out(ctx, ids_out, ids.p, (size_t)K * 4);
+    HM_API_END(ctx)
+}
+
+hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, int32_t r, int32_t K,
+                     int32_t *ids_out, int32_t *count_out) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(layer_ids && ids_out, HM_EINVAL, "null argument");
+    HM_REQUIRE(heuristic == HM_NAIVE || heuristic == HM_CC1 || heuristic == HM_CC2, HM_EINVAL,
+               "unknown heuristic");
+    HM_REQUIRE(r >= 2 && r <= 8, HM_EINVAL, "compose needs 2 <= r <= 8");
+    std::set<int32_t> seen(layer_ids, layer_ids + r);
+    HM_REQUIRE((int32_t)seen.size() == r, HM_EINVAL, "repeated graph id");
+    std::vector<Graph *> gs;
+    for (int i = 0; i < r; ++i) gs.push_back(&graph(ctx, layer_ids[i]));
+    compose(ctx, heuristic, gs, K, ids_out, count_out);
+    HM_API_END(ctx)
+}
+
+hm_status hm_sync(hm_ctx *ctx) {
+    HM_API_BEGIN(ctx)
+    HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    HM_API_END(ctx)
+}
+
+hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(out, HM_EINVAL, "null out");
+    unsigned long long dv[2] = {0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto &pe : ctx->pending) {
+        float ms = 0.f;
+        HM_CUDA(cudaEventElapsedTime(&ms, pe.first, pe.second));
+        ctx->stats.bfs_ms += ms;
+        cudaEventDestroy(pe.first);
+        cudaEventDestroy(pe.second);
+    }
+    ctx->pending.clear();
+    out->launches = ctx->stats.launches;
+    out->bfs_launches = ctx->stats.bfs_launches;
+    out->bfs_ms = ctx->stats.bfs_ms;
+    out->bfs_levels = (int64_t)dv[0];
+    out->bfs_batches = (int64_t)dv[1];
+    if (reset) {
+        ctx->stats = Stats();
+        HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));
+        HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    HM_API_END(ctx)
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// Top-K selection: the K smallest (key, id) pairs of n 64-bit keys, in order.
+//
+// Used by every ranking of the paper's outputs: ground truth by closeness
+// (PAPER.md:205-209), CC2 by estSumDist, CC1 and naive result
+// sets.  Ties go to the lower vertex id, so the
+// composite (key << 32 | id) is unique and the answer is well defined.
+//
+// Radix select over the 96-bit composite, 8 bits per pass from the most
+// significant: per pass a grid histogram of the digit among elements whose
+// higher digits match the prefix found so far, then one small kernel picks
+// the digit holding the K-th element.  After 12 passes the exact K-th
+// composite T is known; every element <= T (exactly K) is gathered and sorted
+// in shared memory (bitonic, K <= 4096) -- larger K use a stable device sort.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hm {
+namespace {
+
+constexpr int TB = 256;
+constexpr int SORT_MAX = 4096;
+
+struct SelState {
+    unsigned long long pkey;   // prefix of key bits found so far
+    unsigned int pid;          // prefix of id bits found so far
+    int rem;                   // rank still to find inside the current prefix group (1-based)
+    unsigned int hist[256];
+    int count;                 // gathered elements
+};
+
+// digit p (0..11) of composite (key, id): p < 8 -> key byte (7-p), else id byte (11-p)
+__device__ __forceinline__ unsigned digit_of(uint64_t key, uint32_t id, int p) {
+    return p < 8 ? (unsigned)((key >> (8 * (7 - p))) & 0xff) : (unsigned)((id >> (8 * (11 - p))) & 0xff);
+}
+
+__device__ __forceinline__ bool prefix_match(uint64_t key, uint32_t id, const SelState &st, int p) {
+    // digits 0..p-1 must match
+    if (p == 0) return true;
+    if (p <= 8) {
+        const int sh = 64 - 8 * p;
+        return (sh >= 64) ? true : ((key >> sh) == (st.pkey >> sh));
+    }
+    if (key != st.pkey) return false;
+    const int sh = 32 - 8 * (p - 8);
+    return (sh >= 32) ? true : ((id >> sh) == (st.pid >> sh));
+}
+
+__global__ void k_hist(const uint64_t *__restrict__ keys, int n, SelState *st, int p) {
+    __shared__ unsigned h[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const SelState s = *st;   // prefix (hist part unused here)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (prefix_match(k, (uint32_t)i, s, p)) atomicAdd(&h[digit_of(k, (uint32_t)i, p)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&st->hist[i], h[i]);
+}
+
+__global__ void k_sel_init(SelState *st, int K) {
+    if (threadIdx.x == 0) st->rem = K;
+}
+
+__global__ void k_pick(SelState *st, int p) {
+    if (threadIdx.x != 0) return;
+    int rem = st->rem;
+    unsigned b = 0;
+    for (; b < 256; ++b) {
+        const int c = (int)st->hist[b];
+        if (rem <= c) break;
+        rem -= c;
+    }
+    if (b > 255) b = 255;   // unreachable when K <= n
+    st->rem = rem;
+    if (p < 8) st->pkey |= (unsigned long long)b << (8 * (7 - p));
+    else st->pid |= b << (8 * (11 - p));
+    for (int i = 0; i < 256; ++i) st->hist[i] = 0;
+}
+
+__global__ void k_gather(const uint64_t *__restrict__ keys, int n, SelState *st, uint64_t *ok, uint32_t *oid) {
+    const uint64_t tk = st->pkey;
+    const uint32_t ti = st->pid;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (k < tk || (k == tk && (uint32_t)i <= ti)) {
+            const int pos = atomicAdd(&st->count, 1);
+            ok[pos] = k;
+            oid[pos] = (uint32_t)i;
+        }
+    }
+}
+
+__device__ __forceinline__ bool less_kv(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// one block, K <= SORT_MAX: bitonic sort of (key, id) then write ids
+__global__ void __launch_bounds__(1024) k_sort_small(const uint64_t *ok, const uint32_t *oid, int K, int P,
+                                                     int32_t *out) {
+    extern __shared__ unsigned char smem[];
+    uint64_t *sk = reinterpret_cast<uint64_t *>(smem);
+    uint32_t *si = reinterpret_cast<uint32_t *>(sk + P);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        sk[i] = i < K ? ok[i] : ~0ull;
+        si[i] = i < K ? oid[i] : 0xffffffffu;
+    }
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool sw = up ? less_kv(sk[j], si[j], sk[i], si[i]) : less_kv(sk[i], si[i], sk[j], si[j]);
+                    if (sw) {
+                        const uint64_t tk = sk[i]; sk[i] = sk[j]; sk[j] = tk;
+                        const uint32_t ti = si[i]; si[i] = si[j]; si[j] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < K; i += blockDim.x) out[i] = (int32_t)si[i];
+}
+
+__global__ void k_iota_u32(uint32_t *p, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = (uint32_t)i;
+}
+__global__ void k_copy_ids(const uint32_t *src, int K, int32_t *out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) out[i] = (int32_t)src[i];
+}
+
+__global__ void k_desc_keys(const double *c, int V, uint64_t *key) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+        key[v] = ~(uint64_t)__double_as_longlong(c[v]);
+}
+
+}  // namespace
+
+void closeness_desc_keys(hm_ctx *ctx, const double *d_c, int32_t V, uint64_t *d_keys) {
+    k_desc_keys<<<grid_for(V, TB, (int64_t)ctx->num_sms * 16), TB, 0, ctx->stream>>>(d_c, V, d_keys);
+    check_launch("k_desc_keys");
+    count_launch(ctx);
+}
+
+void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_ids_out) {
+    cudaStream_t s = ctx->stream;
+    HM_REQUIRE(K >= 1 && K <= n, HM_EINVAL, "top-K needs 1 <= K <= n");
+    if (K > SORT_MAX) {
+        // stable radix sort of all (key, id) pairs; ids ascending on ties
+        Buf ids((size_t)n * 4, s), ko((size_t)n * 8, s), io((size_t)n * 4, s);
+        k_iota_u32<<<grid_for(n, TB), TB, 0, s>>>(ids.as<uint32_t>(), n);
+        size_t tb = 0;
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, d_keys, ko.as<uint64_t>(), ids.as<uint32_t>(),
+                                                io.as<uint32_t>(), n, 0, 64, s));
+        Buf tmp(tb, s);
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, d_keys, ko.as<uint64_t>(), ids.as<uint32_t>(),
+                                                io.as<uint32_t>(), n, 0, 64, s));
+        k_copy_ids<<<grid_for(K, TB), TB, 0, s>>>(io.as<uint32_t>(), K, d_ids_out);
+        check_launch("topk large");
+        count_launch(ctx, 10);
+        return;
+    }
+    Buf stb(sizeof(SelState), s), ok((size_t)K * 8, s), oid((size_t)K * 4, s);
+    SelState *st = stb.as<SelState>();
+    HM_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), s));
+    k_sel_init<<<1, 32, 0, s>>>(st, K);
+    const unsigned g = grid_for(n, TB, (int64_t)ctx->num_sms * 4);
+    for (int p = 0; p < 12; ++p) {
+        k_hist<<<g, TB, 0, s>>>(d_keys, n, st, p);
+        k_pick<<<1, 32, 0, s>>>(st, p);
+    }
+    k_gather<<<g, TB, 0, s>>>(d_keys, n, st, ok.as<uint64_t>(), oid.as<uint32_t>());
+    int P = 1;
+    while (P < K) P <<= 1;
+    const size_t sm = (size_t)P * 12;
+    if (sm > 48 * 1024)
+        HM_CUDA(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_sort_small<<<1, 1024, sm, s>>>(ok.as<uint64_t>(), oid.as<uint32_t>(), K, P, d_ids_out);
+    check_launch("topk");
+    count_launch(ctx, 27);
+}
+
+}  // namespace hm

@@ -1,0 +1,199 @@
+"""Thin Python binding over the C ABI (include/hm.h): argument marshalling only.
+
+Every step of the path -- CSR build, AND/OR aggregation, all-sources BFS
+closeness, exact means, CC-node sets, composition and top-K -- runs in
+libhm.so's CUDA kernels.  PyTorch is used for device memory and the stream.
+
+Inputs may be numpy arrays (host) or torch CUDA tensors (device); outputs are
+returned as numpy arrays by default, or written into caller-supplied torch
+CUDA tensors (``out=``) without leaving the device.
+"""
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import HM_CC1, HM_CC2, HM_NAIVE  # noqa: F401
+
+HEURISTICS = {"naive": HM_NAIVE, "cc1": HM_CC1, "cc2": HM_CC2}
+
+
+class HmError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_lib.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(x):
+    """data pointer of a numpy array or torch tensor (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    # torch tensor
+    assert x.is_contiguous()
+    return x.data_ptr()
+
+
+class Context:
+    """One hm_ctx on ``device``, issuing work on ``stream`` (a torch.cuda.Stream,
+    or None for a fresh torch stream kept in ``self.stream``).  Time or order
+    torch work against the library with ``self.stream``."""
+
+    def __init__(self, device=0, stream=None):
+        self.L = _lib.load()
+        import torch
+        self.torch = torch
+        torch.cuda.init()
+        self.stream = torch.cuda.Stream(device) if stream is None else stream
+        s = self.stream.cuda_stream
+        self._stream = s
+        h = ctypes.c_void_p()
+        st = self.L.hm_create(ctypes.byref(h), int(device), ctypes.c_void_p(s) if s else None)
+        if st != 0:
+            raise HmError(st, "hm_create failed")
+        self.h = h
+        self.device = device
+        self.V = None
+        self.n_layers = 0
+
+    # ------------------------------------------------------------ plumbing
+    def _check(self, st):
+        if st != 0:
+            raise HmError(st, self.L.hm_last_error(self.h).decode(errors="replace"))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.hm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_param(self, name, value):
+        self._check(self.L.hm_set_param(self.h, name.encode(), int(value)))
+
+    def sync(self):
+        self._check(self.L.hm_sync(self.h))
+
+    def stats(self, reset=False):
+        s = _lib.HmStats()
+        self._check(self.L.hm_get_stats(self.h, ctypes.byref(s), 1 if reset else 0))
+        return {k: getattr(s, k) for k, _ in _lib.HmStats._fields_}
+
+    # ------------------------------------------------------------- graphs
+    def load_layers(self, V, layers):
+        """layers: list of (m,2) int32 arrays (numpy host or torch CUDA).
+        Returns (layer ids, dropped counts)."""
+        l = len(layers)
+        keep = []
+        ptrs = (ctypes.c_void_p * l)()
+        ms = (ctypes.c_int64 * l)()
+        for i, E in enumerate(layers):
+            if isinstance(E, np.ndarray):
+                E = np.ascontiguousarray(E, dtype=np.int32).reshape(-1, 2)
+            else:
+                assert E.dtype == self.torch.int32
+                E = E.contiguous().reshape(-1, 2)
+            keep.append(E)
+            ptrs[i] = _ptr(E) if E.shape[0] else None
+            ms[i] = E.shape[0]
+        dropped = (ctypes.c_int64 * l)()
+        self._check(self.L.hm_load_layers(self.h, int(V), l, ptrs, ms, dropped))
+        self.V = int(V)
+        self.n_layers = l
+        return list(range(l)), [int(x) for x in dropped]
+
+    def graph_info(self, g):
+        V = ctypes.c_int32()
+        m = ctypes.c_int64()
+        self._check(self.L.hm_graph_info(self.h, int(g), ctypes.byref(V), ctypes.byref(m), None, None))
+        return V.value, m.value
+
+    def graph_csr(self, g):
+        V, m = self.graph_info(g)
+        rp = np.zeros(V + 1, np.int32)
+        col = np.zeros(max(2 * m, 1), np.int32)
+        self._check(self.L.hm_graph_csr(self.h, int(g), _ptr(rp), _ptr(col)))
+        return rp, col[:2 * m]
+
+    def and_aggregate(self, ids):
+        ids = (ctypes.c_int32 * len(ids))(*ids)
+        out = ctypes.c_int32()
+        self._check(self.L.hm_and_aggregate(self.h, ids, len(ids), ctypes.byref(out)))
+        return out.value
+
+    def or_aggregate(self, ids):
+        ids = (ctypes.c_int32 * len(ids))(*ids)
+        out = ctypes.c_int32()
+        self._check(self.L.hm_or_aggregate(self.h, ids, len(ids), ctypes.byref(out)))
+        return out.value
+
+    def free_graph(self, g):
+        self._check(self.L.hm_free_graph(self.h, int(g)))
+
+    # ----------------------------------------------------------- analysis
+    def closeness(self, g, out=None, want=("S", "k", "c", "pen")):
+        """All-sources BFS closeness of graph g.  Returns dict of numpy arrays
+        (S uint64, k int32, c float64, pen uint64) for the names in ``want``;
+        with ``out`` (dict of torch CUDA tensors) writes there instead."""
+        V, _ = self.graph_info(g)
+        if out is None:
+            res = {}
+            if "S" in want:
+                res["S"] = np.zeros(V, np.uint64)
+            if "k" in want:
+                res["k"] = np.zeros(V, np.int32)
+            if "c" in want:
+                res["c"] = np.zeros(V, np.float64)
+            if "pen" in want:
+                res["pen"] = np.zeros(V, np.uint64)
+        else:
+            res = out
+        self._check(self.L.hm_closeness(self.h, int(g), _ptr(res.get("S")), _ptr(res.get("k")),
+                                        _ptr(res.get("c")), _ptr(res.get("pen"))))
+        return res
+
+    def cc_nodes(self, g):
+        """(sorted numpy array of CC nodes, count, mean closeness)."""
+        V, _ = self.graph_info(g)
+        bm = np.zeros((V + 31) // 32, np.uint32)
+        cnt = ctypes.c_int32()
+        mu = ctypes.c_double()
+        self._check(self.L.hm_cc_nodes(self.h, int(g), _ptr(bm), ctypes.byref(cnt), ctypes.byref(mu)))
+        bits = np.unpackbits(bm.view(np.uint8), bitorder="little")[:V]
+        return np.nonzero(bits)[0].astype(np.int64), cnt.value, mu.value
+
+    def degrees(self, g):
+        V, _ = self.graph_info(g)
+        d = np.zeros(V, np.int32)
+        self._check(self.L.hm_degrees(self.h, int(g), _ptr(d)))
+        return d
+
+    def topk_closeness(self, g, K, out=None):
+        ids = np.zeros(K, np.int32) if out is None else out
+        self._check(self.L.hm_topk_closeness(self.h, int(g), int(K), _ptr(ids)))
+        return ids
+
+    # -------------------------------------------------------- composition
+    def compose(self, heuristic, ids, K, out=None):
+        """heuristic in {'cc1','cc2','naive'}.  Returns (ranked ids, |result set|)."""
+        h = HEURISTICS[heuristic] if isinstance(heuristic, str) else int(heuristic)
+        arr = (ctypes.c_int32 * len(ids))(*ids)
+        buf = np.zeros(K, np.int32) if out is None else out
+        cnt = ctypes.c_int32()
+        self._check(self.L.hm_compose(self.h, h, arr, len(ids), int(K), _ptr(buf), ctypes.byref(cnt)))
+        n = cnt.value
+        if out is None:
+            return buf[:min(K, n)], n
+        return buf, n

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element, on the same seeded inputs.
+
+Bars (BASELINE.json north_star): S, k, pen, AND edge sets, CC-node sets and
+every top-K list bit-exact; closeness within 1e-12 relative (the pinned
+formula is also expected, and asserted, to be bit-exact).
+"""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from synth import build_config, random_graph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hm():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2207_11662_b200 import build as B
+    B.build()
+    from paper_2207_11662_b200 import Context
+    return Context
+
+
+def edges_arr(E):
+    return np.array(sorted(E), dtype=np.int32).reshape(-1, 2)
+
+
+def check_psi(V, E, got, res=None):
+    """compare the GPU closeness outputs with the oracle on (V, E)."""
+    if res is None:
+        res = O.analyze(V, E)
+    assert got["S"].tolist() == res["S"]
+    assert got["k"].tolist() == res["k"]
+    assert got["pen"].tolist() == res["pen"]
+    c_ref = np.array(res["c"], dtype=np.float64)
+    rel = np.abs(got["c"] - c_ref) / np.maximum(np.abs(c_ref), 1e-300)
+    assert np.all(rel <= 1e-12)
+    assert np.array_equal(got["c"].view(np.uint64), c_ref.view(np.uint64))   # bit-exact
+    return res
+
+
+def run_graph(ctx, V, E):
+    ctx.load_layers(V, [edges_arr(E)])
+    return ctx.closeness(0)
+
+
+# ---------------------------------------------------------------------------
+# Psi on small graphs: edge cases and random shapes
+# ---------------------------------------------------------------------------
+def special_graphs():
+    gs = []
+    gs.append(("V1", 1, set()))
+    gs.append(("V2-empty", 2, set()))
+    gs.append(("V2-edge", 2, {(0, 1)}))
+    gs.append(("empty-100", 100, set()))
+    gs.append(("path-1500", 1500, {(i, i + 1) for i in range(1499)}))   # > 1000 levels
+    gs.append(("star-3000", 3000, {(0, i) for i in range(1, 3000)}))    # degree >> 64
+    gs.append(("cycle-777", 777, {(i, (i + 1) % 777) for i in range(777)} | set()))
+    gs.append(("K40", 40, {(u, v) for u in range(40) for v in range(u + 1, 40)}))
+    # two stars + isolated + a path (components of very different size)
+    E = {(0, i) for i in range(1, 200)} | {(300, i) for i in range(301, 340)} | {(i, i + 1) for i in range(500, 900)}
+    gs.append(("mixed-1000", 1000, E))
+    # component exactly B, B+1 and 2B-1 sources (batch-window edges, W=16 -> B=1024)
+    for n in (1024, 1025, 2047, 2049):
+        gs.append((f"path-{n}", n, {(i, i + 1) for i in range(n - 1)}))
+    gs.append(("tree-3000", 3000, {(i, (i - 1) // 2) for i in range(1, 3000)}))
+    return gs
+
+
+@pytest.mark.parametrize("name,V,E", special_graphs(), ids=[g[0] for g in special_graphs()])
+def test_psi_special(hm, name, V, E):
+    E = {(min(u, v), max(u, v)) for u, v in E if u != v}
+    with hm() as ctx:
+        got = run_graph(ctx, V, E)
+        res = check_psi(V, E, got)
+        nodes, cnt, mu = ctx.cc_nodes(0)
+        assert set(nodes.tolist()) == res["CH"] and cnt == len(res["CH"])
+        assert mu == res["mu"]
+        K = min(V, 17)
+        assert ctx.topk_closeness(0, K).tolist() == O.topk_closeness(res["c"], K)
+
+
+def test_psi_random_graphs(hm):
+    rng = random.Random(2022)
+    with hm() as ctx:
+        for t in range(40):
+            V = rng.choice([5, 33, 64, 65, 200, 513, 1000, 2500])
+            m = rng.choice([0, V // 4, V // 2, V, 2 * V, 4 * V])
+            kind = rng.choice(["er", "rmat"])
+            E = {tuple(e) for e in random_graph(V, m, seed=1000 + t, kind=kind).tolist()}
+            got = run_graph(ctx, V, E)
+            res = check_psi(V, E, got)
+            nodes, cnt, mu = ctx.cc_nodes(0)
+            assert set(nodes.tolist()) == res["CH"], (t, V, m, kind)
+            assert mu == res["mu"]
+            assert ctx.degrees(0).tolist() == res["deg"]
+
+
+def test_tuning_invariance(hm):
+    """results do not depend on batch width, heavy-row threshold or grid size."""
+    V = 3000
+    E = {tuple(e) for e in random_graph(V, 6 * V, seed=77, kind="rmat").tolist()}
+    res = O.analyze(V, E)
+    for words in (8, 16, 32):
+        for heavy in (4, 64, 100000):
+            for bps in (0, 1):
+                with hm() as ctx:
+                    ctx.set_param("bfs_words", words)
+                    ctx.set_param("bfs_heavy", heavy)
+                    ctx.set_param("bfs_blocks_per_sm", bps)
+                    check_psi(V, E, run_graph(ctx, V, E), res)
+
+
+def test_loader_canonicalises(hm):
+    """self-loops and duplicates dropped, either direction accepted."""
+    V = 6
+    raw = np.array([[0, 1], [1, 0], [2, 2], [1, 2], [2, 1], [4, 5], [0, 1]], dtype=np.int32)
+    with hm() as ctx:
+        _, dropped = ctx.load_layers(V, [raw])
+        assert dropped == [4]
+        rp, col = ctx.graph_csr(0)
+        assert rp.tolist() == [0, 1, 3, 4, 4, 5, 6]
+        assert col.tolist() == [1, 0, 2, 1, 5, 4]
+
+
+def test_errors(hm):
+    from paper_2207_11662_b200 import HmError
+    with hm() as ctx:
+        with pytest.raises(HmError, match="HM_ERANGE"):
+            ctx.load_layers(4, [np.array([[0, 4]], np.int32)])
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.load_layers(0, [np.zeros((0, 2), np.int32)])
+        ctx.load_layers(5, [np.array([[0, 1]], np.int32), np.array([[0, 1], [1, 2]], np.int32)])
+        with pytest.raises(HmError, match="HM_ESTATE"):
+            ctx.compose("cc2", [0, 1], 2)                 # before closeness
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.and_aggregate([0])
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.and_aggregate([0, 0])
+        with pytest.raises(HmError, match="HM_ESTATE"):
+            ctx.and_aggregate([0, 7])
+        ctx.closeness(0)
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.topk_closeness(0, 6)
+        with pytest.raises(HmError, match="HM_ESTATE"):
+            ctx.free_graph(0)
+        # context stays usable after errors
+        g = ctx.and_aggregate([0, 1])
+        assert ctx.graph_info(g) == (5, 1)
+
+
+# ---------------------------------------------------------------------------
+# full pipeline on HoMLNs: AND, GT top-K, CC1, CC2, naive (exact)
+# ---------------------------------------------------------------------------
+def homln_cases():
+    return [("C1", None), ("C2", 2048), ("C3", 1024), ("C4", 2048), ("C5", 4096)]
+
+
+def run_pipeline_and_compare(ctx, h, check_layers=True):
+    V = h.V
+    ids, _ = ctx.load_layers(V, h.layers)
+    Es = [set(map(tuple, L.tolist())) for L in h.layers]
+    refs = []
+    for i in ids:
+        got = ctx.closeness(i)
+        refs.append(check_psi(V, Es[i], got) if check_layers else O.analyze(V, Es[i]))
+        nodes, _, mu = ctx.cc_nodes(i)
+        assert set(nodes.tolist()) == refs[-1]["CH"] and mu == refs[-1]["mu"]
+    for T in h.subsets:
+        K = min(h.K, V)
+        g = ctx.and_aggregate(list(T))
+        rp, col = ctx.graph_csr(g)
+        A = O.and_aggregate([Es[i] for i in T])
+        src = np.repeat(np.arange(V), np.diff(rp))
+        gotE = {(int(a), int(b)) for a, b in zip(src, col) if a < b}
+        assert gotE == A
+        ra = check_psi(V, A, ctx.closeness(g))
+        assert ctx.topk_closeness(g, K).tolist() == O.topk_closeness(ra["c"], K)
+        rs = [refs[i] for i in T]
+        ids2, n2 = ctx.compose("cc2", list(T), K)
+        assert ids2.tolist() == O.cc2(rs, K)[0] and n2 == K
+        ids1, n1 = ctx.compose("cc1", list(T), K)
+        r1, nr1, _ = O.cc1(rs, K)
+        assert n1 == nr1 and ids1.tolist() == r1
+        idsn, nn = ctx.compose("naive", list(T), K)
+        rn, nrn, _ = O.naive(rs, K)
+        assert nn == nrn and idsn.tolist() == rn
+        ctx.free_graph(g)
+
+
+@pytest.mark.parametrize("name,V", homln_cases(), ids=[f"{n}@{v or 'full'}" for n, v in homln_cases()])
+def test_pipeline_scaled_configs(hm, name, V):
+    h = build_config(name, V=V)
+    with hm() as ctx:
+        run_pipeline_and_compare(ctx, h)
+
+
+def test_cc1_golden_on_gpu(hm):
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cc1_six_vertex.json")))
+    with hm() as ctx:
+        ctx.load_layers(6, [np.array(g["L1"], np.int32), np.array(g["L2"], np.int32)])
+        ctx.closeness(0)
+        ctx.closeness(1)
+        ids, n = ctx.compose("cc1", [0, 1], 6)
+        assert ids.tolist() == g["CC1_ranked"] and n == 4
+        assert ctx.compose("cc2", [0, 1], 3)[0].tolist() == g["CC2_top3"]
+        assert ctx.compose("naive", [0, 1], 6)[0].tolist() == g["naive"]
+        a = ctx.and_aggregate([0, 1])
+        assert ctx.closeness(a)["S"].tolist() == g["AND_S"]
+        assert ctx.topk_closeness(a, 3).tolist() == g["GT_top3"]
+
+
+def test_device_tensors_roundtrip(hm):
+    import torch
+    h = build_config("C5", V=2048)
+    with hm() as ctx:
+        layers = [torch.from_numpy(L).cuda() for L in h.layers]
+        ctx.load_layers(h.V, layers)
+        out = {"S": torch.zeros(h.V, dtype=torch.int64, device="cuda"),
+               "k": torch.zeros(h.V, dtype=torch.int32, device="cuda"),
+               "c": torch.zeros(h.V, dtype=torch.float64, device="cuda"),
+               "pen": torch.zeros(h.V, dtype=torch.int64, device="cuda")}
+        ctx.closeness(0, out=out)
+        ctx.sync()
+        res = O.analyze(h.V, set(map(tuple, h.layers[0].tolist())))
+        assert out["S"].cpu().numpy().astype(np.uint64).tolist() == res["S"]
+        assert out["c"].cpu().numpy().tolist() == res["c"]
+        ids = torch.zeros(10, dtype=torch.int32, device="cuda")
+        ctx.topk_closeness(0, 10, out=ids)
+        ctx.sync()
+        assert ids.cpu().tolist() == O.topk_closeness(res["c"], 10)
