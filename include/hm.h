@@ -64,6 +64,7 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (0 = occupancy maximum)
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
+ *   "bfs_dbg"     : debug bits (1 = per-thread fence before grid barriers, 2 = level counters)
  * Unknown name -> HM_EINVAL. */
 hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value);
 
@@ -167,6 +168,12 @@ typedef struct {
     int64_t bfs_batches;
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
+
+/* Debug: copy the per-level counters of the last MS-BFS launch made with
+ * hm_set_param("bfs_dbg", 2): out[d] = rows changed at level d, out[4096+d] =
+ * CTAs that saw level d's change flag set.  n <= 8192 uint64 (host).  ESTATE
+ * if no such launch happened. */
+hm_status hm_debug_counts(hm_ctx *ctx, uint64_t *out, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,7 @@ SIGNATURES = {
     "hm_topk_closeness": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int32, vp]),
     "hm_compose": (ctypes.c_int32, [vp, ctypes.c_int32, c_i32p, ctypes.c_int32, ctypes.c_int32, vp, c_i32p]),
     "hm_sync": (ctypes.c_int32, [vp]),
+    "hm_debug_counts": (ctypes.c_int32, [vp, vp, ctypes.c_int32]),
     "hm_get_stats": (ctypes.c_int32, [vp, ctypes.POINTER(HmStats), ctypes.c_int]),
 }
 

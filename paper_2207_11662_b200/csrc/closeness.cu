@@ -59,10 +59,13 @@ __global__ void k_cc_union(const int32_t *__restrict__ row_ptr, const int32_t *_
     }
 }
 
-__global__ void k_cc_compress(int32_t *p, int32_t *csize, int V) {
+// Final labels go to a separate array: concurrent path halving inside cc_find
+// may still rewrite parent[] entries (to valid, less-compressed ancestors),
+// so writing roots back into parent[] would race.
+__global__ void k_cc_compress(int32_t *p, int32_t *label, int32_t *csize, int V) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         const int r = cc_find(p, v);
-        p[v] = r;
+        label[v] = r;
         atomicAdd(csize + r, 1);
     }
 }
@@ -204,7 +207,7 @@ void closeness(hm_ctx *ctx, Graph &G) {
         G.ch.alloc((size_t)((V + 31) / 32) * 4 + 8 + 8, s);   // bitmap + mu + count
     }
 
-    Buf label((size_t)V * 4, s), csize((size_t)V * 4, s);
+    Buf parent((size_t)V * 4, s), label((size_t)V * 4, s), csize((size_t)V * 4, s);
     Buf key1((size_t)V * 8, s), key2((size_t)V * 8, s);
     Buf size_s((size_t)V * 4, s), cstart((size_t)V * 4, s), rank((size_t)V * 4, s);
     Buf n2o((size_t)V * 4, s), o2n((size_t)V * 4, s), ndeg((size_t)(V + 1) * 4, s);
@@ -216,9 +219,9 @@ void closeness(hm_ctx *ctx, Graph &G) {
     HM_CUDA(cudaMemsetAsync(csize.p, 0, csize.bytes, s));
 
     // 1. connected components
-    k_iota<<<gb, TB, 0, s>>>(label.as<int32_t>(), V);
-    k_cc_union<<<gw, TB, 0, s>>>(G.row_ptr.as<int32_t>(), G.col.as<int32_t>(), label.as<int32_t>(), V);
-    k_cc_compress<<<gb, TB, 0, s>>>(label.as<int32_t>(), csize.as<int32_t>(), V);
+    k_iota<<<gb, TB, 0, s>>>(parent.as<int32_t>(), V);
+    k_cc_union<<<gw, TB, 0, s>>>(G.row_ptr.as<int32_t>(), G.col.as<int32_t>(), parent.as<int32_t>(), V);
+    k_cc_compress<<<gb, TB, 0, s>>>(parent.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(), V);
     check_launch("cc");
     count_launch(ctx, 3);
 
@@ -259,11 +262,20 @@ void closeness(hm_ctx *ctx, Graph &G) {
     check_launch("k_relabel_cols");
     count_launch(ctx);
 
+    if (ctx->params.bfs_dbg & 2) {
+        if (!ctx->dbgc.p) ctx->dbgc.alloc(335872 * 8, s);
+        const size_t nn = (size_t)(V < 65536 ? V : 65536);
+        HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + 139264 * 8, n2o.p, nn * 4, cudaMemcpyDeviceToDevice, s));
+        HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + (139264 + 65536) * 8, nrp.p, nn * 4,
+                                cudaMemcpyDeviceToDevice, s));
+        HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + (139264 + 2 * 65536) * 8, key2.p, nn * 8,
+                                cudaMemcpyDeviceToDevice, s));
+    }
     // 4. MS-BFS
     const size_t rowb = (size_t)W * 8;
     const size_t bmw = (size_t)(V + 31) / 32 + 1;
     Buf vis((size_t)V * rowb, s), F0((size_t)V * rowb, s), F1((size_t)V * rowb, s);
-    Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), flags(16, s);
+    Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), flags(128, s);
     HM_CUDA(cudaMemsetAsync(Srel.p, 0, Srel.bytes, s));
     HM_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, s));
     BfsArgs a;
@@ -286,7 +298,17 @@ void closeness(hm_ctx *ctx, Graph &G) {
     a.touched = bm + 4 * bmw;
     a.S = Srel.as<uint64_t>();
     a.flags = flags.as<int32_t>();
+    a.bar = reinterpret_cast<unsigned *>(flags.as<int32_t>() + 16);
     a.counters = ctx->dstats.as<unsigned long long>();
+    a.dbg = ctx->params.bfs_dbg;
+    a.dbgc = nullptr;
+    if (ctx->params.bfs_dbg & 2) {
+        if (!ctx->dbgc.p) {
+            ctx->dbgc.alloc(335872 * 8, s);
+        }
+        HM_CUDA(cudaMemsetAsync(ctx->dbgc.p, 0, 139264 * 8, s));
+        a.dbgc = ctx->dbgc.as<unsigned long long>();
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->params.timing) {
         HM_CUDA(cudaEventCreate(&e0));

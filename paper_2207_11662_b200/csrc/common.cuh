@@ -87,6 +87,7 @@ struct Params {
     int bfs_heavy = 256;
     int bfs_blocks_per_sm = 0;
     int timing = 0;
+    int bfs_dbg = 0;
 };
 
 struct Stats {
@@ -106,6 +107,7 @@ struct hm_ctx {
     int32_t n_layers = 0;
     hm::Params params;
     hm::Stats stats;
+    hm::Buf dbgc;             // debug counters of the last MS-BFS launch (bfs_dbg & 2)
     hm::Buf dstats;           // device counters: [0] levels, [1] batches (uint64)
     int num_sms = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;

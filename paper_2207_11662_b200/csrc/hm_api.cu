@@ -102,6 +102,7 @@ void hm_destroy(hm_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->graphs.clear();
     ctx->dstats.release();
+    ctx->dbgc.release();
     for (auto &pe : ctx->pending) {
         cudaEventDestroy(pe.first);
         cudaEventDestroy(pe.second);
@@ -128,6 +129,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_blocks_per_sm") {
         HM_REQUIRE(value >= 0, HM_EINVAL, "bfs_blocks_per_sm must be >= 0");
         ctx->params.bfs_blocks_per_sm = (int)value;
+    } else if (n == "bfs_dbg") {
+        ctx->params.bfs_dbg = (int)value;
     } else if (n == "timing") {
         ctx->params.timing = value ? 1 : 0;
     } else {
@@ -284,6 +287,15 @@ hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, i
     std::vector<Graph *> gs;
     for (int i = 0; i < r; ++i) gs.push_back(&graph(ctx, layer_ids[i]));
     compose(ctx, heuristic, gs, K, ids_out, count_out);
+    HM_API_END(ctx)
+}
+
+hm_status hm_debug_counts(hm_ctx *ctx, uint64_t *out, int32_t n) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(out && n > 0 && n <= 335872, HM_EINVAL, "bad debug buffer");
+    HM_REQUIRE(ctx->dbgc.p, HM_ESTATE, "no debug counters (set bfs_dbg bit 2 and run hm_closeness)");
+    HM_CUDA(cudaMemcpyAsync(out, ctx->dbgc.p, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HM_CUDA(cudaStreamSynchronize(ctx->stream));
     HM_API_END(ctx)
 }
 

@@ -47,6 +47,34 @@ __device__ __forceinline__ void st2(uint64_t *p, ulonglong2 v) {
     *reinterpret_cast<ulonglong2 *>(p) = v;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid barrier on a monotonically increasing arrival counter: generation g is
+// complete when bar[0] reaches gridDim.x * g; the last arriver publishes g in
+// bar[1].  Every thread fences its own writes before arriving and after
+// leaving (release / acquire at gpu scope).
+__device__ __forceinline__ void gbar(unsigned *bar, unsigned &gen) {
+    __threadfence();
+    __syncthreads();
+    ++gen;
+    if (threadIdx.x == 0) {
+        const unsigned target = gen * gridDim.x;
+        const unsigned arrived = atomicAdd(bar, 1u) + 1u;
+        if (arrived == target) {
+            __threadfence();
+            atomicExch(bar + 1, gen);
+        } else {
+            while (ld_acquire_gpu(bar + 1) < gen) __nanosleep(32);
+        }
+    }
+    __syncthreads();
+    __threadfence();
+}
+
 // bits [0, nb) of a B-bit row, restricted to 64-bit word w
 __device__ __forceinline__ uint64_t window_word(int w, int64_t nb) {
     const int64_t lo = (int64_t)w * 64;
@@ -152,6 +180,10 @@ __device__ __forceinline__ void commit_row(const BfsArgs &a, int v, int d, const
         if (!rs.tch) atomicOr(&a.touched[v >> 5], vbit);
         if (complete) atomicOr(&a.done[v >> 5], vbit);
         *flag = 1;
+        if (a.dbgc) {
+            atomicAdd(a.dbgc + (d < 4095 ? d : 4095), 1ull);
+            if (v < 65536 && d < 64) atomicOr(a.dbgc + 8192 + v, 1ull << d);
+        }
     }
 }
 
@@ -161,6 +193,7 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
     constexpr int64_t B = 64 * W;      // sources per batch
     constexpr int TPB = BLOCK / T;     // teams per block
     cg::grid_group grid = cg::this_grid();
+    unsigned int gen = 0;
     __shared__ int s_hi;
     __shared__ ulonglong2 s_red[TPB][T];
 
@@ -184,6 +217,12 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
         if (threadIdx.x == 0) s_hi = batch_hi(a, base, n_comp, n_live);
         __syncthreads();
         const int hi = s_hi;
+        if (a.dbgc && threadIdx.x == 0 && base / B < 64) {
+            atomicMax(a.dbgc + 6000 + base / B, (unsigned long long)hi);
+            if (blockIdx.x == 0 && base == 0) {
+                a.dbgc[6100] = n_live; a.dbgc[6101] = n_giant; a.dbgc[6102] = n_comp; a.dbgc[6103] = n_heavy;
+            }
+        }
         const int64_t nbw = (hi + 31) >> 5;
 
         // ---- level 0: sources of every component window; bitmaps reset
@@ -217,7 +256,8 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
             }
         }
         if (gtid == 0) a.flags[1] = 0;
-        grid.sync();
+        if (a.dbg & 1) __threadfence();
+        if (a.dbg & 32) gbar(a.bar, gen); else grid.sync();
 
         int d = 1;
         for (;; ++d) {
@@ -269,12 +309,13 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
             // ---- light rows: one team per row
             for (int64_t vv = team; vv < hi; vv += nteams) {
                 const int v = (int)vv;
-                if ((a.done[v >> 5] >> (v & 31)) & 1u) continue;         // team-uniform
+                if (!(a.dbg & 8) && ((a.done[v >> 5] >> (v & 31)) & 1u)) continue;         // team-uniform
                 const int rb = a.row_ptr[v], re = a.row_ptr[v + 1];
                 if (re - rb > heavy_deg) continue;
                 ulonglong2 acc = make_ulonglong2(0ull, 0ull);
                 RowState rs;
                 bool have = false;
+                int nm = 0;
                 for (int j0 = rb; j0 < re; j0 += T) {
                     const int j = j0 + tl;
                     int u = 0;
@@ -284,19 +325,33 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                         c = (chp[u >> 5] >> (u & 31)) & 1u;
                     }
                     const unsigned m = __ballot_sync(tmask, c) >> tbase;
+                    nm += __popc(m);
                     if (!m) continue;
                     if (!have) {
                         rs = load_row_state<W>(a, v, base, tl);
                         have = true;
                     }
-                    const bool need = ((acc.x | rs.vv.x) != rs.fw.x) || ((acc.y | rs.vv.y) != rs.fw.y);
+                    const bool need = (a.dbg & 16) || ((acc.x | rs.vv.x) != rs.fw.x) || ((acc.y | rs.vv.y) != rs.fw.y);
                     if (!__any_sync(tmask, need)) break;
                     gather_chunk<W, T>(Fc, m, u, tmask, tbase, tl, need, acc);
                 }
+                if (a.dbgc && d == 1 && v < 65536) {
+                    int ac = __popcll(acc.x) + __popcll(acc.y);
+                    for (int o = T / 2; o > 0; o >>= 1) ac += __shfl_xor_sync(tmask, ac, o);
+                    int fc = __popcll(Fc[(size_t)v * W + 2 * tl]) + __popcll(Fc[(size_t)v * W + 2 * tl + 1]);
+                    for (int o = T / 2; o > 0; o >>= 1) fc += __shfl_xor_sync(tmask, fc, o);
+                    if (tl == 0)
+                        a.dbgc[73728 + v] = 1ull | (have ? 2ull : 0ull) | ((unsigned long long)nm << 8) |
+                                            ((unsigned long long)(re - rb) << 16) | ((unsigned long long)ac << 24) |
+                                            ((unsigned long long)fc << 40) | ((unsigned long long)blockIdx.x << 48);
+                }
                 if (have) commit_row<W, T>(a, v, d, rs, acc, Fn, chn, flag, tmask, tl);
             }
-            grid.sync();
-            if (*((volatile int32_t *)flag) == 0) break;
+            if (a.dbg & 1) __threadfence();
+            if (a.dbg & 32) gbar(a.bar, gen); else grid.sync();
+            const int fv = *((volatile int32_t *)flag);
+            if (a.dbgc && threadIdx.x == 0) atomicAdd(a.dbgc + 4096 + (d < 4095 ? d : 4095), (unsigned long long)fv);
+            if (fv == 0) break;
         }
         if (gtid == 0) {
             a.counters[0] += (unsigned long long)d;

@@ -25,6 +25,9 @@ struct BfsArgs {
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches
+    unsigned long long *dbgc;    // debug: [d] rows changed at level d, [4096+d] blocks that saw the flag set
+    unsigned *bar;               // [2] grid-barrier state (zeroed before launch)
+    int dbg;                     // debug bits: 1 = per-thread fence before each grid barrier
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per

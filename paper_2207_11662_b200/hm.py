@@ -46,8 +46,12 @@ class Context:
         import torch
         self.torch = torch
         torch.cuda.init()
-        self.stream = torch.cuda.Stream(device) if stream is None else stream
-        s = self.stream.cuda_stream
+        if stream is False:          # library-owned stream (debug)
+            self.stream = None
+            s = 0
+        else:
+            self.stream = torch.cuda.Stream(device) if stream is None else stream
+            s = self.stream.cuda_stream
         self._stream = s
         h = ctypes.c_void_p()
         st = self.L.hm_create(ctypes.byref(h), int(device), ctypes.c_void_p(s) if s else None)
@@ -85,6 +89,11 @@ class Context:
 
     def sync(self):
         self._check(self.L.hm_sync(self.h))
+
+    def debug_counts(self, n=335872):
+        out = np.zeros(n, np.uint64)
+        self._check(self.L.hm_debug_counts(self.h, _ptr(out), n))
+        return out
 
     def stats(self, reset=False):
         s = _lib.HmStats()
