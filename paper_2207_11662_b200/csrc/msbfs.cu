@@ -8,20 +8,30 @@
 //
 // Target-side accumulation (exact, undirected graphs): since
 // d(s,v) = d(v,s), summing d * popc(new bits of row v at level d) over all
-// batches gives S(v) directly -- no transpose, one owner per row, no atomics
-// on the sums.
+// batches gives S(v) directly -- no transpose, one owner per row.
 //
 // Work reduction, all exact:
 //  * sources are batched per connected component (rows grouped by component,
 //    components sorted by size descending, isolated vertices excluded); batch
 //    `base` covers every component larger than `base`, each with its own
 //    source window [start+base, start+base+B) -- so a row only ever sees bits
-//    of sources in its own component and "complete" (all window sources
-//    reached) is well defined per row;
+//    of sources in its own component and "complete" is well defined per row;
 //  * a row only gathers from neighbours that changed at the previous level
-//    (row bitmap `chg`, L1-resident), and only the words it still misses;
-//  * complete rows are skipped (bitmap `done`); a row whose neighbours did not
-//    change reads only its column indices.
+//    (row bitmap `chg`), and only the words it still misses;
+//  * complete rows are skipped (bitmap `done`).
+//
+// Level step (one warp per 32-row group; the group's bitmap words belong to
+// that warp for the level):
+//  1. scan: the warp walks the group's arcs 32 at a time, coalesced; each lane
+//     finds its arc's row by a shuffle binary search over the group's row
+//     offsets and keeps arcs whose row is live and whose neighbour changed;
+//     kept (row, neighbour) pairs are staged in shared memory in arc order,
+//     hence grouped by row;
+//  2. gather/commit: the warp's W/2-lane teams take one row segment each, in
+//     lock-step, issue all the segment's 16-byte frontier gathers (4 in
+//     flight), OR them, and commit new = acc & ~vis;
+//  3. the group's chg / done / touched words are published with one atomicOr
+//     each (rows of degree > heavy_deg are handled by whole CTAs first).
 //
 // Memory layout: state rows are W*8 bytes (128 B at W=16), row-major, so a
 // team of W/2 lanes moves one row with 16-byte vector loads -- one L2 line.
@@ -39,40 +49,15 @@ namespace hm {
 namespace {
 
 constexpr int BLOCK = 512;
+constexpr int NWARP = BLOCK / 32;
+constexpr int CAP = 256;           // staged pairs per warp
+constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ ulonglong2 ld2(const uint64_t *p) {
     return *reinterpret_cast<const ulonglong2 *>(p);
 }
 __device__ __forceinline__ void st2(uint64_t *p, ulonglong2 v) {
     *reinterpret_cast<ulonglong2 *>(p) = v;
-}
-
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Grid barrier on a monotonically increasing arrival counter: generation g is
-// complete when bar[0] reaches gridDim.x * g; the last arriver publishes g in
-// bar[1].  Every thread fences its own writes before arriving and after
-// leaving (release / acquire at gpu scope).
-__device__ __forceinline__ void gbar(unsigned *bar, unsigned &gen) {
-    __threadfence();
-    __syncthreads();
-    ++gen;
-    if (threadIdx.x == 0) {
-        const unsigned target = gen * gridDim.x;
-        const unsigned arrived = atomicAdd(bar, 1u) + 1u;
-        if (arrived == target) {
-            __threadfence();
-            atomicExch(bar + 1, gen);
-        } else {
-            while (ld_acquire_gpu(bar + 1) < gen) __nanosleep(32);
-        }
-    }
-    __syncthreads();
-    __threadfence();
 }
 
 // bits [0, nb) of a B-bit row, restricted to 64-bit word w
@@ -100,19 +85,17 @@ __device__ int batch_hi(const BfsArgs &a, int64_t base, int n_comp, int n_live) 
 struct RowState {
     ulonglong2 vv;   // visited bits (lane's 2 words)
     ulonglong2 fw;   // full window mask
-    bool tch;        // vis row valid in global memory
 };
 
 template <int W>
-__device__ __forceinline__ RowState load_row_state(const BfsArgs &a, int v, int64_t base, int tl) {
+__device__ __forceinline__ RowState row_state(const BfsArgs &a, int v, int64_t base, int tl, bool tch) {
     constexpr int64_t B = 64 * W;
     RowState r;
     const int2 ci = a.cinfo[v];
     int64_t nb = (int64_t)ci.y - base;
     if (nb > B) nb = B;
     r.fw = make_ulonglong2(window_word(2 * tl, nb), window_word(2 * tl + 1, nb));
-    r.tch = (a.touched[v >> 5] >> (v & 31)) & 1u;
-    if (r.tch) {
+    if (tch) {
         r.vv = ld2(a.vis + (size_t)v * W + 2 * tl);
     } else {
         r.vv = make_ulonglong2(0ull, 0ull);
@@ -126,85 +109,34 @@ __device__ __forceinline__ RowState load_row_state(const BfsArgs &a, int v, int6
     return r;
 }
 
-// Gather step over one chunk of T neighbour slots: lanes hold candidate
-// neighbour ids `u` (valid where bit set in m, team-relative), each lane loads
-// its 16 bytes of every changed neighbour's frontier row unless the lane's
-// words are already complete.  Up to 4 rows in flight per lane.
-template <int W, int T>
-__device__ __forceinline__ void gather_chunk(const uint64_t *__restrict__ Fc, unsigned m, int u,
-                                             unsigned tmask, int tbase, int tl, bool need,
-                                             ulonglong2 &acc) {
-    while (m) {
-        const int t0 = __ffs(m) - 1;
-        m &= m - 1;
-        int t1 = t0, t2 = t0, t3 = t0;
-        bool h1 = false, h2 = false, h3 = false;
-        if (m) { t1 = __ffs(m) - 1; m &= m - 1; h1 = true; }
-        if (m) { t2 = __ffs(m) - 1; m &= m - 1; h2 = true; }
-        if (m) { t3 = __ffs(m) - 1; m &= m - 1; h3 = true; }
-        const int u0 = __shfl_sync(tmask, u, tbase + t0);
-        const int u1 = __shfl_sync(tmask, u, tbase + t1);
-        const int u2 = __shfl_sync(tmask, u, tbase + t2);
-        const int u3 = __shfl_sync(tmask, u, tbase + t3);
-        if (need) {
-            const ulonglong2 x0 = ld2(Fc + (size_t)u0 * W + 2 * tl);
-            ulonglong2 x1 = make_ulonglong2(0ull, 0ull), x2 = x1, x3 = x1;
-            if (h1) x1 = ld2(Fc + (size_t)u1 * W + 2 * tl);
-            if (h2) x2 = ld2(Fc + (size_t)u2 * W + 2 * tl);
-            if (h3) x3 = ld2(Fc + (size_t)u3 * W + 2 * tl);
-            acc.x |= x0.x | x1.x | x2.x | x3.x;
-            acc.y |= x0.y | x1.y | x2.y | x3.y;
-        }
-    }
-}
-
-// Commit: new = acc & ~vis; write vis/frontier, accumulate S, set bitmaps.
-// Executed by all T lanes of one team (team-uniform control flow).
-template <int W, int T>
-__device__ __forceinline__ void commit_row(const BfsArgs &a, int v, int d, const RowState &rs,
-                                           ulonglong2 acc, uint64_t *__restrict__ Fn,
-                                           uint32_t *chn, int32_t *flag, unsigned tmask, int tl) {
-    const ulonglong2 nw = make_ulonglong2(acc.x & ~rs.vv.x, acc.y & ~rs.vv.y);
-    int cnt = __popcll(nw.x) + __popcll(nw.y);
-#pragma unroll
-    for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(tmask, cnt, o);
-    if (cnt == 0) return;
-    const ulonglong2 nv = make_ulonglong2(rs.vv.x | nw.x, rs.vv.y | nw.y);
-    st2(a.vis + (size_t)v * W + 2 * tl, nv);
-    st2(Fn + (size_t)v * W + 2 * tl, nw);
-    const bool complete = __all_sync(tmask, nv.x == rs.fw.x && nv.y == rs.fw.y);
-    if (tl == 0) {
-        const uint32_t vbit = 1u << (v & 31);
-        a.S[v] += (uint64_t)d * (uint64_t)cnt;
-        atomicOr(&chn[v >> 5], vbit);
-        if (!rs.tch) atomicOr(&a.touched[v >> 5], vbit);
-        if (complete) atomicOr(&a.done[v >> 5], vbit);
-        *flag = 1;
-        if (a.dbgc) {
-            atomicAdd(a.dbgc + (d < 4095 ? d : 4095), 1ull);
-            if (v < 65536 && d < 64) atomicOr(a.dbgc + 8192 + v, 1ull << d);
-        }
-    }
-}
+struct Smem {
+    int hi;
+    int32_t su[NWARP][CAP];         // staged neighbour ids
+    uint8_t sr[NWARP][CAP];         // staged row index within the group
+    int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
+};
 
 template <int W>
 __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2;           // lanes per row
+    constexpr int TPW = 32 / T;        // teams per warp
     constexpr int64_t B = 64 * W;      // sources per batch
     constexpr int TPB = BLOCK / T;     // teams per block
     cg::grid_group grid = cg::this_grid();
-    unsigned int gen = 0;
-    __shared__ int s_hi;
+    __shared__ Smem sm;
     __shared__ ulonglong2 s_red[TPB][T];
 
     const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
     const int tl = lane % T;
+    const int team = lane / T;                  // team within warp
     const int tbase = lane - tl;
-    const unsigned tmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << tbase);
+    const unsigned tmask = (T == 32) ? FULL : (((1u << T) - 1u) << tbase);
+    const unsigned ltmask = (1u << lane) - 1u;
     const int64_t nthreads = (int64_t)gridDim.x * BLOCK;
     const int64_t gtid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-    const int64_t team = gtid / T;
-    const int64_t nteams = nthreads / T;
+    const int64_t gwarp = gtid >> 5;
+    const int64_t nwarps = nthreads >> 5;
     const int tib = threadIdx.x / T;
 
     const int n_live = a.scalars[0];
@@ -212,22 +144,19 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
     const int n_comp = a.scalars[2];
     const int n_heavy = a.scalars[3];
     const int heavy_deg = a.heavy_deg;
+    int32_t *su = sm.su[wib];
+    uint8_t *sr = sm.sr[wib];
+    int16_t *seg = sm.seg[wib];
 
     for (int64_t base = 0; base < n_giant; base += B) {
-        if (threadIdx.x == 0) s_hi = batch_hi(a, base, n_comp, n_live);
+        if (threadIdx.x == 0) sm.hi = batch_hi(a, base, n_comp, n_live);
         __syncthreads();
-        const int hi = s_hi;
-        if (a.dbgc && threadIdx.x == 0 && base / B < 64) {
-            atomicMax(a.dbgc + 6000 + base / B, (unsigned long long)hi);
-            if (blockIdx.x == 0 && base == 0) {
-                a.dbgc[6100] = n_live; a.dbgc[6101] = n_giant; a.dbgc[6102] = n_comp; a.dbgc[6103] = n_heavy;
-            }
-        }
-        const int64_t nbw = (hi + 31) >> 5;
+        const int hi = sm.hi;
+        const int64_t ngroups = (hi + 31) >> 5;
 
         // ---- level 0: sources of every component window; bitmaps reset
-        for (int64_t vb = gtid & ~31LL; vb < hi; vb += nthreads) {
-            const int v = (int)(vb + lane);
+        for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+            const int v = (int)(g * 32 + lane);
             bool src = false, dn = false;
             if (v < hi) {
                 const int2 ci = a.cinfo[v];
@@ -245,19 +174,17 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                                                    w + 1 == wj ? 1ull << (j & 63) : 0ull));
                 }
             }
-            const unsigned bs = __ballot_sync(0xffffffffu, src);
-            const unsigned bd = __ballot_sync(0xffffffffu, dn);
+            const unsigned bs = __ballot_sync(FULL, src);
+            const unsigned bd = __ballot_sync(FULL, dn);
             if (lane == 0) {
-                const int64_t w = vb >> 5;
-                a.chg0[w] = bs;
-                a.chg1[w] = 0u;
-                a.done[w] = bd;
-                a.touched[w] = 0u;
+                a.chg0[g] = bs;
+                a.chg1[g] = 0u;
+                a.done[g] = bd;
+                a.touched[g] = 0u;
             }
         }
         if (gtid == 0) a.flags[1] = 0;
-        if (a.dbg & 1) __threadfence();
-        if (a.dbg & 32) gbar(a.bar, gen); else grid.sync();
+        grid.sync();
 
         int d = 1;
         for (;; ++d) {
@@ -268,7 +195,7 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
             uint32_t *chn = r1 == 0 ? a.chg0 : (r1 == 1 ? a.chg1 : a.chg2);
             uint32_t *chz = r2 == 0 ? a.chg0 : (r2 == 1 ? a.chg1 : a.chg2);
             int32_t *flag = a.flags + r1;
-            for (int64_t w = gtid; w < nbw; w += nthreads) chz[w] = 0u;
+            for (int64_t w = gtid; w < ngroups; w += nthreads) chz[w] = 0u;
             if (gtid == 0) a.flags[r2] = 0;
 
             // ---- heavy rows: one CTA per row, neighbour list split over teams
@@ -277,7 +204,8 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                 if (v >= hi) continue;                                   // block-uniform
                 if ((a.done[v >> 5] >> (v & 31)) & 1u) continue;         // block-uniform
                 const int rb = a.row_ptr[v], re = a.row_ptr[v + 1];
-                const RowState rs = load_row_state<W>(a, v, base, tl);
+                const bool tch = (a.touched[v >> 5] >> (v & 31)) & 1u;
+                const RowState rs = row_state<W>(a, v, base, tl, tch);
                 ulonglong2 acc = make_ulonglong2(0ull, 0ull);
                 for (int j0 = rb + tib * T; j0 < re; j0 += BLOCK) {
                     const int j = j0 + tl;
@@ -287,11 +215,18 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                         u = a.col[j];
                         c = (chp[u >> 5] >> (u & 31)) & 1u;
                     }
-                    const unsigned m = __ballot_sync(tmask, c) >> tbase;
-                    if (!m) continue;
+                    unsigned m = __ballot_sync(tmask, c) >> tbase;
                     const bool need = ((acc.x | rs.vv.x) != rs.fw.x) || ((acc.y | rs.vv.y) != rs.fw.y);
-                    if (!__any_sync(tmask, need)) break;
-                    gather_chunk<W, T>(Fc, m, u, tmask, tbase, tl, need, acc);
+                    while (m) {
+                        const int t0 = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int u0 = __shfl_sync(tmask, u, tbase + t0);
+                        if (need) {
+                            const ulonglong2 x = ld2(Fc + (size_t)u0 * W + 2 * tl);
+                            acc.x |= x.x;
+                            acc.y |= x.y;
+                        }
+                    }
                 }
                 s_red[tib][tl] = acc;
                 __syncthreads();
@@ -301,56 +236,165 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                         acc.x |= x.x;
                         acc.y |= x.y;
                     }
-                    commit_row<W, T>(a, v, d, rs, acc, Fn, chn, flag, tmask, tl);
+                    const ulonglong2 nw = make_ulonglong2(acc.x & ~rs.vv.x, acc.y & ~rs.vv.y);
+                    int cnt = __popcll(nw.x) + __popcll(nw.y);
+#pragma unroll
+                    for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(tmask, cnt, o);
+                    if (cnt) {
+                        const ulonglong2 nv = make_ulonglong2(rs.vv.x | nw.x, rs.vv.y | nw.y);
+                        st2(a.vis + (size_t)v * W + 2 * tl, nv);
+                        st2(Fn + (size_t)v * W + 2 * tl, nw);
+                        const bool complete = __all_sync(tmask, nv.x == rs.fw.x && nv.y == rs.fw.y);
+                        if (tl == 0) {
+                            const uint32_t vbit = 1u << (v & 31);
+                            a.S[v] += (uint64_t)d * (uint64_t)cnt;
+                            atomicOr(&chn[v >> 5], vbit);
+                            if (!tch) atomicOr(&a.touched[v >> 5], vbit);
+                            if (complete) atomicOr(&a.done[v >> 5], vbit);
+                            *flag = 1;
+                        }
+                    }
                 }
                 __syncthreads();
             }
 
-            // ---- light rows: one team per row
-            for (int64_t vv = team; vv < hi; vv += nteams) {
-                const int v = (int)vv;
-                if (!(a.dbg & 8) && ((a.done[v >> 5] >> (v & 31)) & 1u)) continue;         // team-uniform
-                const int rb = a.row_ptr[v], re = a.row_ptr[v + 1];
-                if (re - rb > heavy_deg) continue;
-                ulonglong2 acc = make_ulonglong2(0ull, 0ull);
-                RowState rs;
-                bool have = false;
-                int nm = 0;
-                for (int j0 = rb; j0 < re; j0 += T) {
-                    const int j = j0 + tl;
+            // ---- light rows: one warp per 32-row group
+            for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+                const int r = (int)(g * 32 + lane);
+                const bool valid = r < hi;
+                const int rp = a.row_ptr[valid ? r : hi];
+                const int rnext = __shfl_down_sync(FULL, rp, 1);
+                const int rend = (lane == 31) ? a.row_ptr[r + 1 < hi ? r + 1 : hi] : rnext;
+                const uint32_t dword = a.done[g];
+                const bool act = valid && !((dword >> lane) & 1u) && (rend - rp) <= heavy_deg;
+                const unsigned amask = __ballot_sync(FULL, act);
+                if (!amask) continue;                                    // warp-uniform
+                uint32_t tword = a.touched[g];
+                uint32_t chg_bits = 0u, done_bits = 0u;
+                const int A0 = __shfl_sync(FULL, rp, 0);
+                const int A1 = __shfl_sync(FULL, rend, 31);
+                int n = 0;
+                for (int a0 = A0; a0 < A1; a0 += 32) {
+                    const int aa = a0 + lane;
+                    int lo = 0;
+#pragma unroll
+                    for (int s = 16; s > 0; s >>= 1) {
+                        const int c = lo + s;
+                        const int x = __shfl_sync(FULL, rp, c & 31);
+                        if (c < 32 && x <= aa) lo = c;
+                    }
+                    bool ok = false;
                     int u = 0;
-                    bool c = false;
-                    if (j < re) {
-                        u = a.col[j];
-                        c = (chp[u >> 5] >> (u & 31)) & 1u;
+                    if (aa < A1 && ((amask >> lo) & 1u)) {
+                        u = a.col[aa];
+                        ok = (chp[u >> 5] >> (u & 31)) & 1u;
                     }
-                    const unsigned m = __ballot_sync(tmask, c) >> tbase;
-                    nm += __popc(m);
-                    if (!m) continue;
-                    if (!have) {
-                        rs = load_row_state<W>(a, v, base, tl);
-                        have = true;
+                    const unsigned bm = __ballot_sync(FULL, ok);
+                    if (ok) {
+                        const int pos = n + __popc(bm & ltmask);
+                        su[pos] = u;
+                        sr[pos] = (uint8_t)lo;
                     }
-                    const bool need = (a.dbg & 16) || ((acc.x | rs.vv.x) != rs.fw.x) || ((acc.y | rs.vv.y) != rs.fw.y);
-                    if (!__any_sync(tmask, need)) break;
-                    gather_chunk<W, T>(Fc, m, u, tmask, tbase, tl, need, acc);
+                    n += __popc(bm);
+                    const bool flush = (n > CAP - 32) || (a0 + 32 >= A1);
+                    if (flush && n > 0) {
+                        __syncwarp();
+                        // segments: runs of equal row index
+                        int nseg = 0;
+                        for (int k0 = 0; k0 < n; k0 += 32) {
+                            const int k = k0 + lane;
+                            const bool st = k < n && (k == 0 || sr[k] != sr[k - 1]);
+                            const unsigned sb = __ballot_sync(FULL, st);
+                            if (st) seg[nseg + __popc(sb & ltmask)] = (int16_t)k;
+                            nseg += __popc(sb);
+                        }
+                        if (lane == 0) seg[nseg] = (int16_t)n;
+                        __syncwarp();
+                        // teams take segments in lock-step rounds
+                        for (int s0 = 0; s0 < nseg; s0 += TPW) {
+                            const int si = s0 + team;
+                            const bool has = si < nseg;
+                            const int kb = has ? seg[si] : 0;
+                            const int ke = has ? seg[si + 1] : 0;
+                            const int ri = has ? sr[kb] : 0;
+                            const int v = (int)(g * 32 + ri);
+                            const bool tch = (tword >> ri) & 1u;
+                            RowState rs;
+                            ulonglong2 acc = make_ulonglong2(0ull, 0ull);
+                            if (has) rs = row_state<W>(a, v, base, tl, tch);
+                            uint64_t Sv = 0;
+                            if (has && tl == 0) Sv = a.S[v];
+                            // round length: longest segment among the warp's teams
+                            int len = ke - kb;
+#pragma unroll
+                            for (int o = T; o < 32; o <<= 1) len = max(len, __shfl_xor_sync(FULL, len, o));
+                            for (int k = 0; k < len; k += 4) {
+                                const int k0 = kb + k;
+                                const bool need = has && (((acc.x | rs.vv.x) != rs.fw.x) ||
+                                                          ((acc.y | rs.vv.y) != rs.fw.y));
+                                ulonglong2 x0 = make_ulonglong2(0ull, 0ull), x1 = x0, x2 = x0, x3 = x0;
+                                if (need) {
+                                    if (k0 < ke) x0 = ld2(Fc + (size_t)su[k0] * W + 2 * tl);
+                                    if (k0 + 1 < ke) x1 = ld2(Fc + (size_t)su[k0 + 1] * W + 2 * tl);
+                                    if (k0 + 2 < ke) x2 = ld2(Fc + (size_t)su[k0 + 2] * W + 2 * tl);
+                                    if (k0 + 3 < ke) x3 = ld2(Fc + (size_t)su[k0 + 3] * W + 2 * tl);
+                                }
+                                acc.x |= x0.x | x1.x | x2.x | x3.x;
+                                acc.y |= x0.y | x1.y | x2.y | x3.y;
+                            }
+                            // commit
+                            ulonglong2 nw = make_ulonglong2(0ull, 0ull);
+                            if (has) nw = make_ulonglong2(acc.x & ~rs.vv.x, acc.y & ~rs.vv.y);
+                            int cnt = __popcll(nw.x) + __popcll(nw.y);
+#pragma unroll
+                            for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+                            bool complete = false;
+                            if (cnt) {
+                                const ulonglong2 nv = make_ulonglong2(rs.vv.x | nw.x, rs.vv.y | nw.y);
+                                st2(a.vis + (size_t)v * W + 2 * tl, nv);
+                                ulonglong2 fw_out = nw;
+                                if ((chg_bits >> ri) & 1u) {     // row split over staging flushes:
+                                    const ulonglong2 f0 = ld2(Fn + (size_t)v * W + 2 * tl);   // merge
+                                    fw_out.x |= f0.x;
+                                    fw_out.y |= f0.y;
+                                }
+                                st2(Fn + (size_t)v * W + 2 * tl, fw_out);
+                                complete = nv.x == rs.fw.x && nv.y == rs.fw.y;
+                                if (tl == 0) a.S[v] = Sv + (uint64_t)d * (uint64_t)cnt;
+                            }
+                            // team-wide "complete" and warp-wide bit merge
+                            unsigned cflag = complete ? 1u : 0u;
+#pragma unroll
+                            for (int o = T / 2; o > 0; o >>= 1) cflag &= __shfl_xor_sync(FULL, cflag, o);
+                            uint32_t cb = (cnt && tl == 0) ? (1u << ri) : 0u;
+                            uint32_t db = (cnt && tl == 0 && cflag) ? (1u << ri) : 0u;
+#pragma unroll
+                            for (int o = T; o < 32; o <<= 1) {
+                                cb |= __shfl_xor_sync(FULL, cb, o);
+                                db |= __shfl_xor_sync(FULL, db, o);
+                            }
+                            cb = __shfl_sync(FULL, cb, 0);
+                            db = __shfl_sync(FULL, db, 0);
+                            chg_bits |= cb;
+                            done_bits |= db;
+                            tword |= cb;
+                        }
+                        n = 0;
+                        __syncwarp();
+                    }
                 }
-                if (a.dbgc && d == 1 && v < 65536) {
-                    int ac = __popcll(acc.x) + __popcll(acc.y);
-                    for (int o = T / 2; o > 0; o >>= 1) ac += __shfl_xor_sync(tmask, ac, o);
-                    int fc = __popcll(Fc[(size_t)v * W + 2 * tl]) + __popcll(Fc[(size_t)v * W + 2 * tl + 1]);
-                    for (int o = T / 2; o > 0; o >>= 1) fc += __shfl_xor_sync(tmask, fc, o);
-                    if (tl == 0)
-                        a.dbgc[73728 + v] = 1ull | (have ? 2ull : 0ull) | ((unsigned long long)nm << 8) |
-                                            ((unsigned long long)(re - rb) << 16) | ((unsigned long long)ac << 24) |
-                                            ((unsigned long long)fc << 40) | ((unsigned long long)blockIdx.x << 48);
+                if (lane == 0) {
+                    if (chg_bits) {
+                        atomicOr(&chn[g], chg_bits);
+                        atomicOr(&a.touched[g], chg_bits);
+                        *flag = 1;
+                    }
+                    if (done_bits) atomicOr(&a.done[g], done_bits);
                 }
-                if (have) commit_row<W, T>(a, v, d, rs, acc, Fn, chn, flag, tmask, tl);
             }
-            if (a.dbg & 1) __threadfence();
-            if (a.dbg & 32) gbar(a.bar, gen); else grid.sync();
+            grid.sync();
             const int fv = *((volatile int32_t *)flag);
-            if (a.dbgc && threadIdx.x == 0) atomicAdd(a.dbgc + 4096 + (d < 4095 ? d : 4095), (unsigned long long)fv);
+            if (a.dbgc && gtid == 0) a.dbgc[d < 4095 ? d : 4095] += 1ull;
             if (fv == 0) break;
         }
         if (gtid == 0) {
