@@ -136,7 +136,9 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
         const int old = new_to_old[i];
         const int rb = row_ptr[old], re = row_ptr[old + 1];
         const int ob = nrp[i];
-        for (int j = rb + lane; j < re; j += 32) ncol[ob + (j - rb)] = old_to_new[col[j]];
+        // packed arc: (relabelled neighbour << 5) | (row index within its 32-row group)
+        for (int j = rb + lane; j < re; j += 32)
+            ncol[ob + (j - rb)] = (old_to_new[col[j]] << 5) | (int)(i & 31);
         if (lane == 0 && re - rb > heavy_deg) heavy[atomicAdd(scalars + 3, 1)] = (int)i;
     }
 }
@@ -192,6 +194,7 @@ inline int nbits(uint64_t x) {
 void closeness(hm_ctx *ctx, Graph &G) {
     cudaStream_t s = ctx->stream;
     const int V = G.V;
+    HM_REQUIRE(V < (1 << 26), HM_ERANGE, "hm_closeness supports V < 2^26 (packed arc format)");
     const int W = ctx->params.bfs_words;
     const unsigned gb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
     const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
@@ -273,9 +276,9 @@ void closeness(hm_ctx *ctx, Graph &G) {
     }
     // 4. MS-BFS
     const size_t rowb = (size_t)W * 8;
-    const size_t bmw = (size_t)(V + 31) / 32 + 1;
-    Buf vis((size_t)V * rowb, s), F0((size_t)V * rowb, s), F1((size_t)V * rowb, s);
-    Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), flags(128, s);
+    const size_t bmw = (((size_t)(V + 31) / 32) + 4) & ~(size_t)3;   // multiple of 4 words (16-B rows for uint4 copies)
+    Buf F0((size_t)V * rowb, s), F1((size_t)V * rowb, s), F2((size_t)V * rowb, s);
+    Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), Kb((size_t)V * 2 + 16, s), flags(128, s);
     HM_CUDA(cudaMemsetAsync(Srel.p, 0, Srel.bytes, s));
     HM_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, s));
     BfsArgs a;
@@ -287,20 +290,18 @@ void closeness(hm_ctx *ctx, Graph &G) {
     a.scalars = scalars;
     a.heavy = heavy.as<int32_t>();
     a.heavy_deg = ctx->params.bfs_heavy;
-    a.vis = vis.as<uint64_t>();
-    a.F0 = F0.as<uint64_t>();
-    a.F1 = F1.as<uint64_t>();
+    a.F[0] = F0.as<uint64_t>();
+    a.F[1] = F1.as<uint64_t>();
+    a.F[2] = F2.as<uint64_t>();
     uint32_t *bm = bms.as<uint32_t>();
-    a.chg0 = bm;
-    a.chg1 = bm + bmw;
-    a.chg2 = bm + 2 * bmw;
-    a.done = bm + 3 * bmw;
-    a.touched = bm + 4 * bmw;
+    for (int i = 0; i < 4; ++i) a.chg[i] = bm + i * bmw;
+    a.done = bm + 4 * bmw;
+    a.K = Kb.as<uint16_t>();
+    a.chg_words = (int)bmw;
+    a.chg_smem = (bmw * 4 * 2 <= 80 * 1024) ? 1 : 0;
     a.S = Srel.as<uint64_t>();
     a.flags = flags.as<int32_t>();
-    a.bar = reinterpret_cast<unsigned *>(flags.as<int32_t>() + 16);
     a.counters = ctx->dstats.as<unsigned long long>();
-    a.dbg = ctx->params.bfs_dbg;
     a.dbgc = nullptr;
     if (ctx->params.bfs_dbg & 2) {
         if (!ctx->dbgc.p) {

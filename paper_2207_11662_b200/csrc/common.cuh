@@ -83,7 +83,7 @@ struct Graph {
 };
 
 struct Params {
-    int bfs_words = 16;
+    int bfs_words = 32;
     int bfs_heavy = 256;
     int bfs_blocks_per_sm = 0;
     int timing = 0;

@@ -10,33 +10,37 @@
 // d(s,v) = d(v,s), summing d * popc(new bits of row v at level d) over all
 // batches gives S(v) directly -- no transpose, one owner per row.
 //
+// No visited array.  On an undirected graph a source s in
+//   acc_d(v) = OR over neighbours u of F_{d-1}(u)
+// has d(s,u) = d-1 for some neighbour u, hence d(s,v) in {d-2, d-1, d}; so
+//   new_d(v) = acc_d(v) & ~F_{d-1}(v) & ~F_{d-2}(v)
+// is exactly the set of sources at distance d.  A row therefore reads only
+// its own two previous frontier rows (F_{d-1} is the array being gathered,
+// hot in L2) and writes one frontier row per change.  Completion (every
+// window source reached) comes from a 16-bit per-row count K.
+//
 // Work reduction, all exact:
 //  * sources are batched per connected component (rows grouped by component,
 //    components sorted by size descending, isolated vertices excluded); batch
 //    `base` covers every component larger than `base`, each with its own
-//    source window [start+base, start+base+B) -- so a row only ever sees bits
-//    of sources in its own component and "complete" is well defined per row;
+//    source window [start+base, start+base+B);
 //  * a row only gathers from neighbours that changed at the previous level
-//    (row bitmap `chg`), and only the words it still misses;
+//    (row bitmaps staged in shared memory each level);
 //  * complete rows are skipped (bitmap `done`).
 //
-// Level step (one warp per 32-row group; the group's bitmap words belong to
-// that warp for the level):
-//  1. scan: the warp walks the group's arcs 32 at a time, coalesced; each lane
-//     finds its arc's row by a shuffle binary search over the group's row
-//     offsets and keeps arcs whose row is live and whose neighbour changed;
-//     kept (row, neighbour) pairs are staged in shared memory in arc order,
-//     hence grouped by row;
-//  2. gather/commit: the warp's W/2-lane teams take one row segment each, in
-//     lock-step, issue all the segment's 16-byte frontier gathers (4 in
-//     flight), OR them, and commit new = acc & ~vis;
-//  3. the group's chg / done / touched words are published with one atomicOr
-//     each (rows of degree > heavy_deg are handled by whole CTAs first).
+// Level step (one warp per 32-row group, groups claimed dynamically inside a
+// CTA's contiguous range):
+//  1. scan: packed arcs (neighbour << 5 | row in group), SCAN_U x 32 at a time,
+//     coalesced; pairs (row, changed neighbour) staged in shared memory in arc
+//     order, hence grouped by row;
+//  2. gather/commit: the row segments are sorted by length and dealt to the
+//     warp's W/2-lane teams in lock-step rounds; each row's state and frontier
+//     gathers are issued together (16 B per lane per row), OR-ed, committed;
+//  3. the group's chg / done words are published with one atomicOr each
+//     (rows of degree > heavy_deg are handled by whole CTAs first).
 //
-// Memory layout: state rows are W*8 bytes (128 B at W=16), row-major, so a
-// team of W/2 lanes moves one row with 16-byte vector loads -- one L2 line.
-// The frontier array read by the gathers (n_live * W * 8 bytes, 33.5 MB at
-// V=2^18, W=16) stays L2-resident (126 MB).
+// Memory layout: frontier rows are W*8 bytes (256 B at W=32), row-major, so a
+// team of W/2 lanes moves one row with 16-byte vector loads.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -51,6 +55,7 @@ namespace {
 constexpr int BLOCK = 512;
 constexpr int NWARP = BLOCK / 32;
 constexpr int CAP = 256;           // staged pairs per warp
+constexpr int SCAN_U = 4;          // arc chunks (of 32) loaded per scan step
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ ulonglong2 ld2(const uint64_t *p) {
@@ -59,13 +64,10 @@ __device__ __forceinline__ ulonglong2 ld2(const uint64_t *p) {
 __device__ __forceinline__ void st2(uint64_t *p, ulonglong2 v) {
     *reinterpret_cast<ulonglong2 *>(p) = v;
 }
-
-// bits [0, nb) of a B-bit row, restricted to 64-bit word w
-__device__ __forceinline__ uint64_t window_word(int w, int64_t nb) {
-    const int64_t lo = (int64_t)w * 64;
-    if (nb <= lo) return 0ull;
-    if (nb >= lo + 64) return ~0ull;
-    return (1ull << (nb - lo)) - 1ull;
+__device__ __forceinline__ int ld_cs(const int32_t *p) {   // arcs: read once per level
+    int v;
+    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
 }
 
 // first row of the first component with size <= max(base, 1), clamped to n_live
@@ -81,36 +83,16 @@ __device__ int batch_hi(const BfsArgs &a, int64_t base, int n_comp, int n_live) 
     return r < n_live ? r : n_live;
 }
 
-// Per-row context for one lane of a team (2 words per lane).
-struct RowState {
-    ulonglong2 vv;   // visited bits (lane's 2 words)
-    ulonglong2 fw;   // full window mask
-};
-
-template <int W>
-__device__ __forceinline__ RowState row_state(const BfsArgs &a, int v, int64_t base, int tl, bool tch) {
-    constexpr int64_t B = 64 * W;
-    RowState r;
-    const int2 ci = a.cinfo[v];
-    int64_t nb = (int64_t)ci.y - base;
-    if (nb > B) nb = B;
-    r.fw = make_ulonglong2(window_word(2 * tl, nb), window_word(2 * tl + 1, nb));
-    if (tch) {
-        r.vv = ld2(a.vis + (size_t)v * W + 2 * tl);
-    } else {
-        r.vv = make_ulonglong2(0ull, 0ull);
-        const int64_t j = (int64_t)v - ci.x - base;
-        if (j >= 0 && j < nb) {
-            const int wj = (int)(j >> 6);
-            if (wj == 2 * tl) r.vv.x = 1ull << (j & 63);
-            else if (wj == 2 * tl + 1) r.vv.y = 1ull << (j & 63);
-        }
-    }
-    return r;
+// Component of row v: rows [0, n_giant) are the largest component.
+__device__ __forceinline__ int2 comp_of(const BfsArgs &a, int v, int n_giant) {
+    return v < n_giant ? make_int2(0, n_giant) : a.cinfo[v];
 }
+
+__device__ __forceinline__ bool bit_of(const uint32_t *bm, int v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
 
 struct Smem {
     int hi;
+    int next;                       // next group to claim in this CTA's range
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
     int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
@@ -125,13 +107,14 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ Smem sm;
     __shared__ ulonglong2 s_red[TPB][T];
+    extern __shared__ uint4 s_dyn[];
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int tl = lane % T;
     const int team = lane / T;                  // team within warp
     const int tbase = lane - tl;
-    const unsigned tmask = (T == 32) ? FULL : (((1u << T) - 1u) << tbase);
+    const unsigned tmask = ((T == 32) ? FULL : ((1u << T) - 1u)) << tbase;
     const unsigned ltmask = (1u << lane) - 1u;
     const int64_t nthreads = (int64_t)gridDim.x * BLOCK;
     const int64_t gtid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
@@ -140,7 +123,7 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
     const int tib = threadIdx.x / T;
 
     const int n_live = a.scalars[0];
-    const int64_t n_giant = a.scalars[1];
+    const int n_giant = a.scalars[1];
     const int n_comp = a.scalars[2];
     const int n_heavy = a.scalars[3];
     const int heavy_deg = a.heavy_deg;
@@ -154,78 +137,94 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
         const int hi = sm.hi;
         const int64_t ngroups = (hi + 31) >> 5;
 
-        // ---- level 0: sources of every component window; bitmaps reset
+        // ---- level 0: sources of every component window (F_0); bitmaps and counts reset
         for (int64_t g = gwarp; g < ngroups; g += nwarps) {
             const int v = (int)(g * 32 + lane);
             bool src = false, dn = false;
             if (v < hi) {
-                const int2 ci = a.cinfo[v];
+                const int2 ci = comp_of(a, v, n_giant);
                 const int64_t j = (int64_t)v - ci.x - base;
                 int64_t nb = (int64_t)ci.y - base;
                 if (nb > B) nb = B;
                 if (j >= 0 && j < nb) {
                     src = true;
                     dn = (nb == 1);
-                    uint64_t *f = a.F0 + (size_t)v * W;
+                    uint64_t *f = a.F[0] + (size_t)v * W;
                     const int wj = (int)(j >> 6);
 #pragma unroll
                     for (int w = 0; w < W; w += 2)
                         st2(f + w, make_ulonglong2(w == wj ? 1ull << (j & 63) : 0ull,
                                                    w + 1 == wj ? 1ull << (j & 63) : 0ull));
                 }
+                a.K[v] = 0;
             }
             const unsigned bs = __ballot_sync(FULL, src);
             const unsigned bd = __ballot_sync(FULL, dn);
             if (lane == 0) {
-                a.chg0[g] = bs;
-                a.chg1[g] = 0u;
+                a.chg[0][g] = bs;     // changed at level 0: the sources
+                a.chg[1][g] = 0u;     // written at level 1
+                a.chg[3][g] = 0u;     // "level -1" (read as F_{d-2} at level 1)
                 a.done[g] = bd;
-                a.touched[g] = 0u;
             }
         }
         if (gtid == 0) a.flags[1] = 0;
         grid.sync();
 
         int d = 1;
+        unsigned long long t_prev = 0;
+        if (a.dbgc && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
         for (;; ++d) {
-            const uint64_t *__restrict__ Fc = (d & 1) ? a.F0 : a.F1;
-            uint64_t *__restrict__ Fn = (d & 1) ? a.F1 : a.F0;
-            const int r0 = (d - 1) % 3, r1 = d % 3, r2 = (d + 1) % 3;
-            const uint32_t *chp = r0 == 0 ? a.chg0 : (r0 == 1 ? a.chg1 : a.chg2);
-            uint32_t *chn = r1 == 0 ? a.chg0 : (r1 == 1 ? a.chg1 : a.chg2);
-            uint32_t *chz = r2 == 0 ? a.chg0 : (r2 == 1 ? a.chg1 : a.chg2);
-            int32_t *flag = a.flags + r1;
+            const uint64_t *__restrict__ Fc = a.F[(d + 2) % 3];    // F_{d-1}: gathered
+            const uint64_t *__restrict__ Fp = a.F[(d + 1) % 3];    // F_{d-2}: own rows only
+            uint64_t *__restrict__ Fn = a.F[d % 3];                // F_d: written
+            const uint32_t *chp = a.chg[(d + 3) & 3];
+            const uint32_t *chpp = a.chg[(d + 2) & 3];
+            uint32_t *chn = a.chg[d & 3];
+            uint32_t *chz = a.chg[(d + 1) & 3];
+            int32_t *flag = a.flags + (d % 3);
             for (int64_t w = gtid; w < ngroups; w += nthreads) chz[w] = 0u;
-            if (gtid == 0) a.flags[r2] = 0;
+            if (gtid == 0) a.flags[(d + 1) % 3] = 0;
+            // stage the two previous change bitmaps in shared memory
+            const uint32_t *chp_s = chp, *chpp_s = chpp;
+            if (threadIdx.x == 0) sm.next = (int)(((int64_t)blockIdx.x * ngroups) / gridDim.x);
+            if (a.chg_smem) {
+                const int nw4 = (int)((ngroups + 3) >> 2);
+                uint4 *d0 = s_dyn;
+                uint4 *d1 = s_dyn + (a.chg_words >> 2);
+                const uint4 *s0 = reinterpret_cast<const uint4 *>(chp);
+                const uint4 *s1 = reinterpret_cast<const uint4 *>(chpp);
+                for (int i = threadIdx.x; i < nw4; i += BLOCK) {
+                    d0[i] = s0[i];
+                    d1[i] = s1[i];
+                }
+                chp_s = reinterpret_cast<const uint32_t *>(d0);
+                chpp_s = reinterpret_cast<const uint32_t *>(d1);
+            }
+            __syncthreads();
 
             // ---- heavy rows: one CTA per row, neighbour list split over teams
             for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
                 const int v = a.heavy[h];
                 if (v >= hi) continue;                                   // block-uniform
-                if ((a.done[v >> 5] >> (v & 31)) & 1u) continue;         // block-uniform
+                if (bit_of(a.done, v)) continue;                         // block-uniform
                 const int rb = a.row_ptr[v], re = a.row_ptr[v + 1];
-                const bool tch = (a.touched[v >> 5] >> (v & 31)) & 1u;
-                const RowState rs = row_state<W>(a, v, base, tl, tch);
                 ulonglong2 acc = make_ulonglong2(0ull, 0ull);
                 for (int j0 = rb + tib * T; j0 < re; j0 += BLOCK) {
                     const int j = j0 + tl;
                     int u = 0;
                     bool c = false;
                     if (j < re) {
-                        u = a.col[j];
-                        c = (chp[u >> 5] >> (u & 31)) & 1u;
+                        u = a.col[j] >> 5;
+                        c = bit_of(chp_s, u);
                     }
                     unsigned m = __ballot_sync(tmask, c) >> tbase;
-                    const bool need = ((acc.x | rs.vv.x) != rs.fw.x) || ((acc.y | rs.vv.y) != rs.fw.y);
                     while (m) {
                         const int t0 = __ffs(m) - 1;
                         m &= m - 1;
                         const int u0 = __shfl_sync(tmask, u, tbase + t0);
-                        if (need) {
-                            const ulonglong2 x = ld2(Fc + (size_t)u0 * W + 2 * tl);
-                            acc.x |= x.x;
-                            acc.y |= x.y;
-                        }
+                        const ulonglong2 x = ld2(Fc + (size_t)u0 * W + 2 * tl);
+                        acc.x |= x.x;
+                        acc.y |= x.y;
                     }
                 }
                 s_red[tib][tl] = acc;
@@ -236,21 +235,30 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                         acc.x |= x.x;
                         acc.y |= x.y;
                     }
-                    const ulonglong2 nw = make_ulonglong2(acc.x & ~rs.vv.x, acc.y & ~rs.vv.y);
+                    ulonglong2 vv = make_ulonglong2(0ull, 0ull);
+                    if (bit_of(chp_s, v)) vv = ld2(Fc + (size_t)v * W + 2 * tl);
+                    if (bit_of(chpp_s, v)) {
+                        const ulonglong2 x = ld2(Fp + (size_t)v * W + 2 * tl);
+                        vv.x |= x.x;
+                        vv.y |= x.y;
+                    }
+                    const ulonglong2 nw = make_ulonglong2(acc.x & ~vv.x, acc.y & ~vv.y);
                     int cnt = __popcll(nw.x) + __popcll(nw.y);
 #pragma unroll
                     for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(tmask, cnt, o);
                     if (cnt) {
-                        const ulonglong2 nv = make_ulonglong2(rs.vv.x | nw.x, rs.vv.y | nw.y);
-                        st2(a.vis + (size_t)v * W + 2 * tl, nv);
                         st2(Fn + (size_t)v * W + 2 * tl, nw);
-                        const bool complete = __all_sync(tmask, nv.x == rs.fw.x && nv.y == rs.fw.y);
                         if (tl == 0) {
-                            const uint32_t vbit = 1u << (v & 31);
+                            const int2 ci = comp_of(a, v, n_giant);
+                            int64_t nb = (int64_t)ci.y - base;
+                            if (nb > B) nb = B;
+                            const int64_t j = (int64_t)v - ci.x - base;
+                            const int kn = (int)a.K[v] + cnt;
+                            a.K[v] = (uint16_t)kn;
                             a.S[v] += (uint64_t)d * (uint64_t)cnt;
+                            const uint32_t vbit = 1u << (v & 31);
                             atomicOr(&chn[v >> 5], vbit);
-                            if (!tch) atomicOr(&a.touched[v >> 5], vbit);
-                            if (complete) atomicOr(&a.done[v >> 5], vbit);
+                            if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) atomicOr(&a.done[v >> 5], vbit);
                             *flag = 1;
                         }
                     }
@@ -258,135 +266,149 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                 __syncthreads();
             }
 
-            // ---- light rows: one warp per 32-row group
-            for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+            // ---- light rows: one warp per 32-row group; each CTA owns a contiguous
+            // range of groups and its warps claim them dynamically (load balance)
+            const int64_t g_end = ((int64_t)(blockIdx.x + 1) * ngroups) / gridDim.x;
+            for (;;) {
+                int64_t g = 0;
+                if (lane == 0) g = (int64_t)atomicAdd(&sm.next, 1);
+                g = __shfl_sync(FULL, g, 0);
+                if (g >= g_end) break;
                 const int r = (int)(g * 32 + lane);
                 const bool valid = r < hi;
                 const int rp = a.row_ptr[valid ? r : hi];
-                const int rnext = __shfl_down_sync(FULL, rp, 1);
-                const int rend = (lane == 31) ? a.row_ptr[r + 1 < hi ? r + 1 : hi] : rnext;
+                const int rlast = a.row_ptr[(int)(g * 32 + 32) < hi ? (int)(g * 32 + 32) : hi];
                 const uint32_t dword = a.done[g];
+                const int rnext = __shfl_down_sync(FULL, rp, 1);
+                const int rend = (lane == 31) ? rlast : rnext;
                 const bool act = valid && !((dword >> lane) & 1u) && (rend - rp) <= heavy_deg;
                 const unsigned amask = __ballot_sync(FULL, act);
                 if (!amask) continue;                                    // warp-uniform
-                uint32_t tword = a.touched[g];
+                const uint32_t pword = chp_s[g], ppword = chpp_s[g];
                 uint32_t chg_bits = 0u, done_bits = 0u;
                 const int A0 = __shfl_sync(FULL, rp, 0);
-                const int A1 = __shfl_sync(FULL, rend, 31);
+                const int A1 = rlast;
                 int n = 0;
-                for (int a0 = A0; a0 < A1; a0 += 32) {
-                    const int aa = a0 + lane;
-                    int lo = 0;
+                for (int a0 = A0; a0 < A1; a0 += 32 * SCAN_U) {
+                    int xx[SCAN_U];
 #pragma unroll
-                    for (int s = 16; s > 0; s >>= 1) {
-                        const int c = lo + s;
-                        const int x = __shfl_sync(FULL, rp, c & 31);
-                        if (c < 32 && x <= aa) lo = c;
+                    for (int q = 0; q < SCAN_U; ++q) {
+                        const int aa = a0 + 32 * q + lane;
+                        xx[q] = aa < A1 ? ld_cs(a.col + aa) : -1;
                     }
-                    bool ok = false;
-                    int u = 0;
-                    if (aa < A1 && ((amask >> lo) & 1u)) {
-                        u = a.col[aa];
-                        ok = (chp[u >> 5] >> (u & 31)) & 1u;
-                    }
-                    const unsigned bm = __ballot_sync(FULL, ok);
-                    if (ok) {
-                        const int pos = n + __popc(bm & ltmask);
-                        su[pos] = u;
-                        sr[pos] = (uint8_t)lo;
-                    }
-                    n += __popc(bm);
-                    const bool flush = (n > CAP - 32) || (a0 + 32 >= A1);
-                    if (flush && n > 0) {
-                        __syncwarp();
-                        // segments: runs of equal row index
-                        int nseg = 0;
-                        for (int k0 = 0; k0 < n; k0 += 32) {
-                            const int k = k0 + lane;
-                            const bool st = k < n && (k == 0 || sr[k] != sr[k - 1]);
-                            const unsigned sb = __ballot_sync(FULL, st);
-                            if (st) seg[nseg + __popc(sb & ltmask)] = (int16_t)k;
-                            nseg += __popc(sb);
+#pragma unroll
+                    for (int q = 0; q < SCAN_U; ++q) {
+                        const int x = xx[q];
+                        const int u = x >> 5, ri = x & 31;
+                        const bool ok = x >= 0 && ((amask >> ri) & 1u) && bit_of(chp_s, u);
+                        const unsigned bm = __ballot_sync(FULL, ok);
+                        if (ok) {
+                            const int pos = n + __popc(bm & ltmask);
+                            su[pos] = u;
+                            sr[pos] = (uint8_t)ri;
                         }
-                        if (lane == 0) seg[nseg] = (int16_t)n;
-                        __syncwarp();
-                        // teams take segments in lock-step rounds
-                        for (int s0 = 0; s0 < nseg; s0 += TPW) {
-                            const int si = s0 + team;
-                            const bool has = si < nseg;
-                            const int kb = has ? seg[si] : 0;
-                            const int ke = has ? seg[si + 1] : 0;
-                            const int ri = has ? sr[kb] : 0;
-                            const int v = (int)(g * 32 + ri);
-                            const bool tch = (tword >> ri) & 1u;
-                            RowState rs;
-                            ulonglong2 acc = make_ulonglong2(0ull, 0ull);
-                            if (has) rs = row_state<W>(a, v, base, tl, tch);
-                            uint64_t Sv = 0;
-                            if (has && tl == 0) Sv = a.S[v];
-                            // round length: longest segment among the warp's teams
-                            int len = ke - kb;
-#pragma unroll
-                            for (int o = T; o < 32; o <<= 1) len = max(len, __shfl_xor_sync(FULL, len, o));
-                            for (int k = 0; k < len; k += 4) {
-                                const int k0 = kb + k;
-                                const bool need = has && (((acc.x | rs.vv.x) != rs.fw.x) ||
-                                                          ((acc.y | rs.vv.y) != rs.fw.y));
-                                ulonglong2 x0 = make_ulonglong2(0ull, 0ull), x1 = x0, x2 = x0, x3 = x0;
-                                if (need) {
-                                    if (k0 < ke) x0 = ld2(Fc + (size_t)su[k0] * W + 2 * tl);
-                                    if (k0 + 1 < ke) x1 = ld2(Fc + (size_t)su[k0 + 1] * W + 2 * tl);
-                                    if (k0 + 2 < ke) x2 = ld2(Fc + (size_t)su[k0 + 2] * W + 2 * tl);
-                                    if (k0 + 3 < ke) x3 = ld2(Fc + (size_t)su[k0 + 3] * W + 2 * tl);
-                                }
-                                acc.x |= x0.x | x1.x | x2.x | x3.x;
-                                acc.y |= x0.y | x1.y | x2.y | x3.y;
-                            }
-                            // commit
-                            ulonglong2 nw = make_ulonglong2(0ull, 0ull);
-                            if (has) nw = make_ulonglong2(acc.x & ~rs.vv.x, acc.y & ~rs.vv.y);
-                            int cnt = __popcll(nw.x) + __popcll(nw.y);
-#pragma unroll
-                            for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-                            bool complete = false;
-                            if (cnt) {
-                                const ulonglong2 nv = make_ulonglong2(rs.vv.x | nw.x, rs.vv.y | nw.y);
-                                st2(a.vis + (size_t)v * W + 2 * tl, nv);
-                                ulonglong2 fw_out = nw;
-                                if ((chg_bits >> ri) & 1u) {     // row split over staging flushes:
-                                    const ulonglong2 f0 = ld2(Fn + (size_t)v * W + 2 * tl);   // merge
-                                    fw_out.x |= f0.x;
-                                    fw_out.y |= f0.y;
-                                }
-                                st2(Fn + (size_t)v * W + 2 * tl, fw_out);
-                                complete = nv.x == rs.fw.x && nv.y == rs.fw.y;
-                                if (tl == 0) a.S[v] = Sv + (uint64_t)d * (uint64_t)cnt;
-                            }
-                            // team-wide "complete" and warp-wide bit merge
-                            unsigned cflag = complete ? 1u : 0u;
-#pragma unroll
-                            for (int o = T / 2; o > 0; o >>= 1) cflag &= __shfl_xor_sync(FULL, cflag, o);
-                            uint32_t cb = (cnt && tl == 0) ? (1u << ri) : 0u;
-                            uint32_t db = (cnt && tl == 0 && cflag) ? (1u << ri) : 0u;
-#pragma unroll
-                            for (int o = T; o < 32; o <<= 1) {
-                                cb |= __shfl_xor_sync(FULL, cb, o);
-                                db |= __shfl_xor_sync(FULL, db, o);
-                            }
-                            cb = __shfl_sync(FULL, cb, 0);
-                            db = __shfl_sync(FULL, db, 0);
-                            chg_bits |= cb;
-                            done_bits |= db;
-                            tword |= cb;
-                        }
-                        n = 0;
-                        __syncwarp();
+                        n += __popc(bm);
                     }
+                    const bool flush = (n > CAP - 32 * SCAN_U) || (a0 + 32 * SCAN_U >= A1);
+                    if (!flush || n == 0) continue;
+                    __syncwarp();
+                    // segments: runs of equal row index (at most 32)
+                    int nseg = 0;
+                    for (int k0 = 0; k0 < n; k0 += 32) {
+                        const int k = k0 + lane;
+                        const bool st = k < n && (k == 0 || sr[k] != sr[k - 1]);
+                        const unsigned sb = __ballot_sync(FULL, st);
+                        if (st) seg[nseg + __popc(sb & ltmask)] = (int16_t)k;
+                        nseg += __popc(sb);
+                    }
+                    if (lane == 0) seg[nseg] = (int16_t)n;
+                    __syncwarp();
+                    // sort the segments by length (descending) so the TPW rows of a
+                    // lock-step round have similar neighbour counts
+                    int key = lane < nseg ? (((seg[lane + 1] - seg[lane]) << 5) | lane) : -1;
+#pragma unroll
+                    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                        for (int j = k >> 1; j > 0; j >>= 1) {
+                            const int other = __shfl_xor_sync(FULL, key, j);
+                            const bool keep_max = (((lane & k) == 0) == ((lane & j) == 0));
+                            key = keep_max ? max(key, other) : min(key, other);
+                        }
+                    }
+                    uint32_t cb_team = 0u, db_team = 0u;   // per-team-leader bits of this flush
+                    for (int s0 = 0; s0 < nseg; s0 += TPW) {
+                        const int mykey = __shfl_sync(FULL, key, (s0 + team) & 31);
+                        const int rlen = __shfl_sync(FULL, key, s0) >> 5;        // longest in round
+                        const bool has = s0 + team < nseg;
+                        const int sg = mykey & 31;
+                        const int kb = has ? seg[sg] : 0;
+                        const int ke = has ? seg[sg + 1] : 0;
+                        const int ri = has ? sr[kb] : 0;
+                        const int v = (int)(g * 32 + ri);
+                        // row state, issued with the gathers: own F_{d-1}, F_{d-2}, K, S
+                        ulonglong2 vv = make_ulonglong2(0ull, 0ull), v2 = vv;
+                        if (has && ((pword >> ri) & 1u)) vv = ld2(Fc + (size_t)v * W + 2 * tl);
+                        if (has && ((ppword >> ri) & 1u)) v2 = ld2(Fp + (size_t)v * W + 2 * tl);
+                        int Kv = 0;
+                        uint64_t Sv = 0;
+                        if (has && tl == 0) {
+                            Kv = a.K[v];
+                            Sv = a.S[v];
+                        }
+                        ulonglong2 acc = make_ulonglong2(0ull, 0ull);
+                        for (int k0 = kb; k0 < kb + rlen; k0 += 4) {
+                            ulonglong2 x0 = make_ulonglong2(0ull, 0ull), x1 = x0, x2 = x0, x3 = x0;
+                            if (k0 < ke) x0 = ld2(Fc + (size_t)su[k0] * W + 2 * tl);
+                            if (k0 + 1 < ke) x1 = ld2(Fc + (size_t)su[k0 + 1] * W + 2 * tl);
+                            if (k0 + 2 < ke) x2 = ld2(Fc + (size_t)su[k0 + 2] * W + 2 * tl);
+                            if (k0 + 3 < ke) x3 = ld2(Fc + (size_t)su[k0 + 3] * W + 2 * tl);
+                            acc.x |= x0.x | x1.x | x2.x | x3.x;
+                            acc.y |= x0.y | x1.y | x2.y | x3.y;
+                        }
+                        vv.x |= v2.x;
+                        vv.y |= v2.y;
+                        // a row split over staging flushes already wrote part of F_d(v)
+                        ulonglong2 f0 = make_ulonglong2(0ull, 0ull);
+                        if (has && ((chg_bits >> ri) & 1u)) {
+                            f0 = ld2(Fn + (size_t)v * W + 2 * tl);
+                            vv.x |= f0.x;
+                            vv.y |= f0.y;
+                        }
+                        const ulonglong2 nw = make_ulonglong2(acc.x & ~vv.x, acc.y & ~vv.y);
+                        int cnt = __popcll(nw.x) + __popcll(nw.y);
+#pragma unroll
+                        for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+                        if (cnt) {
+                            st2(Fn + (size_t)v * W + 2 * tl, make_ulonglong2(nw.x | f0.x, nw.y | f0.y));
+                            if (tl == 0) {
+                                const int2 ci = comp_of(a, v, n_giant);
+                                int64_t nb = (int64_t)ci.y - base;
+                                if (nb > B) nb = B;
+                                const int64_t j = (int64_t)v - ci.x - base;
+                                const int kn = Kv + cnt;
+                                a.K[v] = (uint16_t)kn;
+                                a.S[v] = Sv + (uint64_t)d * (uint64_t)cnt;
+                                cb_team |= 1u << ri;
+                                if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) db_team |= 1u << ri;
+                            }
+                        }
+                    }
+                    // merge the team leaders' bits: warp-uniform
+#pragma unroll
+                    for (int o = T; o < 32; o <<= 1) {
+                        cb_team |= __shfl_xor_sync(FULL, cb_team, o);
+                        db_team |= __shfl_xor_sync(FULL, db_team, o);
+                    }
+                    cb_team = __shfl_sync(FULL, cb_team, 0);
+                    db_team = __shfl_sync(FULL, db_team, 0);
+                    chg_bits |= cb_team;
+                    done_bits |= db_team;
+                    n = 0;
+                    __syncwarp();
                 }
                 if (lane == 0) {
                     if (chg_bits) {
                         atomicOr(&chn[g], chg_bits);
-                        atomicOr(&a.touched[g], chg_bits);
                         *flag = 1;
                     }
                     if (done_bits) atomicOr(&a.done[g], done_bits);
@@ -394,7 +416,14 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
             }
             grid.sync();
             const int fv = *((volatile int32_t *)flag);
-            if (a.dbgc && gtid == 0) a.dbgc[d < 4095 ? d : 4095] += 1ull;
+            if (a.dbgc && gtid == 0) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                const int di = d < 4095 ? d : 4095;
+                a.dbgc[di] += 1ull;
+                a.dbgc[4096 + di] += now - t_prev;
+                t_prev = now;
+            }
             if (fv == 0) break;
         }
         if (gtid == 0) {
@@ -414,14 +443,16 @@ int launch_msbfs(int W, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaSt
         case 32: kern = (const void *)msbfs_kernel<32>; break;
         default: return -1;
     }
+    const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 * 2 : 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) return -5;
     int maxb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, BLOCK, 0) != cudaSuccess) return -2;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, BLOCK, dyn) != cudaSuccess) return -2;
     if (maxb < 1) return -3;
     const int b = (blocks_per_sm > 0 && blocks_per_sm < maxb) ? blocks_per_sm : maxb;
     const int grid = num_sms * b;
     BfsArgs args = a;
     void *kargs[] = {(void *)&args};
-    if (cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(BLOCK), kargs, 0, s) != cudaSuccess) return -4;
+    if (cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(BLOCK), kargs, dyn, s) != cudaSuccess) return -4;
     return grid;
 }
 

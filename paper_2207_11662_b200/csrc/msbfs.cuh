@@ -10,24 +10,23 @@ namespace hm {
 // component, components sorted by size descending (see closeness.cu).
 struct BfsArgs {
     const int32_t *row_ptr;      // relabelled CSR (rows >= n_live have degree 0)
-    const int32_t *col;
+    const int32_t *col;          // packed arcs: (neighbour << 5) | (row & 31)
     const int2 *cinfo;           // per live row: (first row of its component, component size)
     const int32_t *comp_size;    // per component rank (descending sizes)
     const int32_t *comp_start;   // per component rank: first row
     const int32_t *scalars;      // [0] n_live, [1] n_giant (largest size), [2] n_comp, [3] n_heavy
     const int32_t *heavy;        // rows with degree > heavy_deg (any order)
     int32_t heavy_deg;
-    uint64_t *vis;               // [n_live][W]  visited bits (valid where "touched")
-    uint64_t *F0, *F1;           // [n_live][W]  frontier (new bits of the level), ping-pong
-    uint32_t *chg0, *chg1, *chg2;  // row bitmaps: row changed at a level (3-way rotation)
+    uint64_t *F[3];              // [n_live][W] frontier rows of levels d, d-1, d-2 (rotating)
+    uint32_t *chg[4];            // row bitmaps "changed at level", rotating over 4 levels
     uint32_t *done;              // row bitmap: all sources of the row's window reached it
-    uint32_t *touched;           // row bitmap: vis row has been written in this batch
+    uint16_t *K;                 // [n_live] window sources reached so far in this batch (self excluded)
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches
-    unsigned long long *dbgc;    // debug: [d] rows changed at level d, [4096+d] blocks that saw the flag set
-    unsigned *bar;               // [2] grid-barrier state (zeroed before launch)
-    int dbg;                     // debug bits: 1 = per-thread fence before each grid barrier
+    unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times
+    int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
+    int chg_words;               // bitmap words (multiple of 4)
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per
