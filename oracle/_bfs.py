@@ -34,6 +34,13 @@ def lib():
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_num_threads.argtypes = [ctypes.c_int]
+        L.oracle_graph_new.restype = ctypes.c_void_p
+        L.oracle_graph_new.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_graph_free.restype = None
+        L.oracle_graph_free.argtypes = [ctypes.c_void_p]
+        L.oracle_graph_bfs.restype = ctypes.c_int
+        L.oracle_graph_bfs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         _lib = L
     return _lib
 
@@ -59,3 +66,35 @@ def bfs_sources(V, E, sources, threads=0):
     if rc != 0:
         raise RuntimeError(f"oracle_bfs_sources failed: {rc}")
     return S, k
+
+
+class Graph:
+    """Adjacency built once; ``bfs(sources)`` returns (S, k, seconds of the BFS loop)."""
+
+    def __init__(self, V, E):
+        arr = np.ascontiguousarray(E, dtype=np.int32).reshape(-1, 2)
+        self._eu = np.ascontiguousarray(arr[:, 0])
+        self._ev = np.ascontiguousarray(arr[:, 1])
+        self.V = int(V)
+        self.h = lib().oracle_graph_new(self.V, int(len(arr)), self._eu.ctypes.data, self._ev.ctypes.data)
+        if not self.h:
+            raise RuntimeError("oracle_graph_new failed")
+
+    def bfs(self, sources, threads=0):
+        src = np.ascontiguousarray(sources, dtype=np.int32)
+        S = np.zeros(len(src), np.uint64)
+        k = np.zeros(len(src), np.int32)
+        secs = ctypes.c_double(0.0)
+        rc = lib().oracle_graph_bfs(self.h, src.ctypes.data, int(len(src)), S.ctypes.data, k.ctypes.data,
+                                    int(threads), ctypes.byref(secs))
+        if rc != 0:
+            raise RuntimeError(f"oracle_graph_bfs failed: {rc}")
+        return S, k, secs.value
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().oracle_graph_free(self.h)
+                self.h = None
+        except Exception:
+            pass
