@@ -158,7 +158,7 @@ def test_errors(hm):
 # full pipeline on HoMLNs: AND, GT top-K, CC1, CC2, naive (exact)
 # ---------------------------------------------------------------------------
 def homln_cases():
-    return [("C1", None), ("C2", 2048), ("C3", 1024), ("C4", 2048), ("C5", 4096)]
+    return [("C1", None), ("C2", 2048), ("C2", None), ("C3", 1024), ("C4", 2048), ("C5", 4096)]
 
 
 def run_pipeline_and_compare(ctx, h, check_layers=True):
