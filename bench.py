@@ -91,6 +91,23 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# cross-rank aggregation (replicas: every rank runs its own HoMLN)
+# ---------------------------------------------------------------------------
+def job_value(units_local, ms_local, device="cpu"):
+    """Whole-job throughput: units summed over ranks / max-over-ranks time.
+    Returns (value, max_ms).  Single process: units / ms."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return units_local / (ms_local / 1e3), ms_local
+    u = torch.tensor([float(units_local)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(ms_local)], dtype=torch.float64, device=device)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(u.item()) / (float(t.item()) / 1e3), float(t.item())
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
@@ -181,13 +198,8 @@ def run_ours(args, rank, world, local_rank):
     ms = [a.elapsed_time(b) for a, b in times]
     st = ctx.stats(reset=True)
     total_ms = float(sum(ms))
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    value, total_ms = job_value(W_total * args.steps, total_ms, device=f"cuda:{dev}")
     ms_per_step = total_ms / args.steps
-    value = W_total * world / (ms_per_step / 1e3)
 
     # ---- e2e: host edge lists -> public API -> host results, copies inside the timed region
     e2e = None
@@ -219,12 +231,8 @@ def run_ours(args, rank, world, local_rank):
             e_ms.append(e0.elapsed_time(e1))
             d2h = sum(int(o.nbytes) for o in outs)
         e2e_ms = float(np.mean(e_ms))
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": W_total * world / (e2e_ms / 1e3), "unit": "TEPS", "h2d_bytes_per_step": h2d,
+        e2e_val, e2e_ms = job_value(W_total, e2e_ms, device=f"cuda:{dev}")
+        e2e = {"value": e2e_val, "unit": "TEPS", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
     # ---- roofline of the MS-BFS kernel
