@@ -138,6 +138,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.load_layers(V, dev_layers)
     units = []
     graph_names = []
+    arcs_and = []
     for i in range(len(h.layers)):
         r = ctx.closeness(i, want=("k",))
         d = ctx.degrees(i)
@@ -149,18 +150,24 @@ def run_ours(args, rank, world, local_rank):
         d = ctx.degrees(g)
         units.append(int((r["k"].astype(np.int64) * d.astype(np.int64)).sum() // 2))
         graph_names.append("AND" + "".join(map(str, T)))
+        arcs_and.append(2 * ctx.graph_info(g)[1])
         ctx.free_graph(g)
     W_total = sum(units)
-    arcs = []
-    for i in range(len(h.layers)):
-        arcs.append(2 * ctx.graph_info(i)[1])
+    arcs = [2 * ctx.graph_info(i)[1] for i in range(len(h.layers))] + arcs_and
 
     def hot_step():
-        for i in range(len(h.layers)):
-            ctx.closeness(i, out={})
+        if (not args.fused):
+            for i in range(len(h.layers)):
+                ctx.closeness(i, out={})
+        ands = []
         for T in h.subsets:
             g = ctx.and_aggregate(list(T))
-            ctx.closeness(g, out={})
+            if (not args.fused):
+                ctx.closeness(g, out={})
+            ands.append(g)
+        if not (not args.fused):            # layers + ground-truth graphs in one fused MS-BFS pass (--fused)
+            ctx.closeness_multi(list(range(len(h.layers))) + ands)
+        for T, g in zip(h.subsets, ands):
             ctx.topk_closeness(g, K, out=ids_dev)
             ctx.compose("cc2", list(T), K, out=ids_dev)
             ctx.compose("cc1", list(T), K, out=ids_dev)
@@ -216,11 +223,13 @@ def run_ours(args, rank, world, local_rank):
             e0.record(s)
             ctx.load_layers(V, host_layers)                 # H2D from pinned host memory
             outs = []
-            for i in range(len(h.layers)):
-                ctx.closeness(i, out={})
-            for T in h.subsets:
-                g = ctx.and_aggregate(list(T))
-                ctx.closeness(g, out={})
+            ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+            if (not args.fused):
+                for g in list(range(len(h.layers))) + ands:
+                    ctx.closeness(g, out={})
+            else:
+                ctx.closeness_multi(list(range(len(h.layers))) + ands)
+            for T, g in zip(h.subsets, ands):
                 outs.append(ctx.topk_closeness(g, K))       # D2H of every result list
                 outs.append(ctx.compose("cc2", list(T), K)[0])
                 outs.append(ctx.compose("cc1", list(T), K)[0])
@@ -248,16 +257,20 @@ def run_ours(args, rank, world, local_rank):
     bfs_ms_avg = st["bfs_ms"] / n_bfs
     levels_per_launch = st["bfs_levels"] / n_bfs
     Rb = args.words * 8
-    # SURVEY §8(d) dense-level model per level: 4(V+1) row_ptr + 4A col + 3 R V state;
-    # A = mean arcs over the graphs closed in a step
-    A_mean = float(np.mean(arcs))
-    model_bytes = levels_per_launch * (4 * (V + 1) + 4 * A_mean + 3 * Rb * V)
+    # SURVEY §8(d) dense-level model per level: 4(V+1) row_ptr + 4A col + 3 R V state,
+    # with V and A those of one launch (the union of all graphs when fused)
+    if (not args.fused):
+        Vl, Al = V, float(np.mean(arcs))
+    else:
+        Vl, Al = V * len(arcs), float(np.sum(arcs))
+    model_bytes = levels_per_launch * (4 * (Vl + 1) + 4 * Al + 3 * Rb * Vl)
     achieved = model_bytes / (bfs_ms_avg / 1e3) / 1e9 if bfs_ms_avg > 0 else 0.0
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
             "frac": achieved / peak_gbs, "traffic": None, "peak_source": peak_src,
             "kernel": "msbfs_kernel", "bytes_model": "SURVEY 8(d) dense-level: L*(4(V+1)+4A+3RV)",
             "bytes_per_launch": model_bytes, "ms_per_launch": bfs_ms_avg,
-            "levels_per_launch": levels_per_launch, "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9)}
+            "levels_per_launch": levels_per_launch, "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9),
+            "launch_rows": Vl, "launch_arcs": Al, "fused_graphs": 1 if (not args.fused) else len(arcs)}
     launches_per_step = st["launches"] / args.steps
 
     line = {
@@ -383,6 +396,7 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--words", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     args = ap.parse_args()

@@ -44,7 +44,7 @@ enum {
     HM_ESTATE = -5    /* unknown / freed graph id, compose before closeness, free of a layer              */
 };
 
-enum { HM_NAIVE = 0, HM_CC1 = 1, HM_CC2 = 2 };   /* hm_compose heuristics */
+enum { HM_NAIVE = 0, HM_CC1 = 1, HM_CC2 = 2, HM_CC2_AVG = 3 };   /* hm_compose heuristics */
 
 /* ---------------------------------------------------------------- context */
 
@@ -60,7 +60,7 @@ void hm_destroy(hm_ctx *ctx);
 const char *hm_last_error(const hm_ctx *ctx);
 
 /* Tuning knobs (results never depend on them):
- *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16 or 32; sources per batch = 64*words)
+ *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16, 32 or 64; sources per batch = 64*words)
  *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (0 = occupancy maximum)
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
@@ -118,6 +118,21 @@ hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
 hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
                        double *closeness, uint64_t *pen_sum);
 
+/* hm_closeness for n >= 1 distinct graphs in ONE fused pass: the graphs are
+ * independent problems (the layers of a HoMLN, analysed "in parallel",
+ * PAPER.md:142, plus any aggregate), so their all-sources BFS runs over the
+ * disjoint union and shares every level step.  Results are per graph,
+ * identical to n separate hm_closeness calls, cached for hm_compose /
+ * hm_topk_closeness / hm_cc_nodes and readable with hm_closeness_results.
+ * graph_ids: host array.  Errors: n < 1 or repeated id -> EINVAL; unknown id
+ * -> ESTATE; sum of V >= 2^26 -> ERANGE. */
+hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n);
+
+/* Copy the cached hm_closeness results of graph g (ESTATE if none); the same
+ * four outputs as hm_closeness, each NULL-able, host or device, length V. */
+hm_status hm_closeness_results(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
+                               double *closeness, uint64_t *pen_sum);
+
 /* CC nodes of graph g (needs hm_closeness(g) first, else ESTATE):
  * bitmap (ceil(V/32) uint32 words, bit v%32 of word v/32; host or device, may
  * be NULL), *count (may be NULL) and *mean = mu (host, may be NULL). */
@@ -145,9 +160,24 @@ hm_status hm_topk_closeness(hm_ctx *ctx, int32_t g, int32_t K, int32_t *ids_out)
  *           min(K, |R|) ids, *count_out = |R|.
  *   HM_NAIVE: intersection of the CC-node sets, ranked by id;
  *           writes min(K, |R|) ids, *count_out = |R|.
+ *   HM_CC2_AVG ("above average" form of CC2): score(v) =
+ *           (V-1)/est(v) (Eq. 1, binary64, 0 if est == 0); R = {v : score(v) >
+ *           mean score}, the mean being the correctly rounded sum / V; ids
+ *           ascending; writes min(K, |R|) ids, *count_out = |R|.
  * 1 <= K <= V.  ids_out host or device; count_out host (may be NULL). */
 hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, int32_t r,
                      int32_t K, int32_t *ids_out, int32_t *count_out);
+
+/* Accuracy of an estimated CC-node list against the ground truth
+ * (§6: precision, recall, F1; Jaccard similarity): est_ids[n_est]
+ * and gt_ids[n_gt] are vertex ids (host or device; duplicates count once; n = 0
+ * allowed, the pointer may then be NULL).  out (host, 7 doubles) receives
+ * Jaccard |A∩B|/|A∪B| (1 if both empty), precision |A∩B|/|A| (1 if both empty,
+ * 0 if only A is empty), recall |A∩B|/|B| (1 if B empty), F1 2PR/(P+R) (0 if
+ * P+R == 0), then |A|, |B|, |A∩B|.  Each ratio is one IEEE binary64 division.
+ * Errors: V <= 0 or n < 0 -> EINVAL; an id outside [0, V) -> ERANGE. */
+hm_status hm_set_metrics(hm_ctx *ctx, int32_t V, const int32_t *est_ids, int64_t n_est,
+                         const int32_t *gt_ids, int64_t n_gt, double *out);
 
 /* ------------------------------------------------------------ utilities */
 

@@ -1,4 +1,4 @@
-// Psi for one graph (PAPER.md:121-122 §3; :209 §4): all-sources BFS closeness.
+// Psi (PAPER.md:121-122 §3; :209 §4): all-sources BFS closeness of one graph or of several graphs in one fused pass.
 //
 // Pipeline (all device-side, stream-ordered, no host synchronisation):
 //   1. connected components (lock-free union-find, hooks larger root under
@@ -143,14 +143,24 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
     }
 }
 
+// union CSR of several graphs: graph g's vertex v becomes voff + v
+__global__ void k_union_copy(const int32_t *__restrict__ rp, const int32_t *__restrict__ col, int V, int64_t nnz,
+                             int voff, int64_t aoff, int32_t *rp_u, int32_t *col_u) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= V; i += (int64_t)gridDim.x * blockDim.x)
+        rp_u[voff + i] = (int32_t)(rp[i] + aoff);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
+        col_u[aoff + j] = col[j] + voff;
+}
+
+// per-graph finalize; union arrays are indexed at voff + v
 __global__ void k_finalize(const int32_t *old_to_new, const int32_t *label, const int32_t *csize,
                            const int32_t *row_ptr, const uint64_t *S_rel, const int32_t *scalars,
-                           uint64_t *S, int32_t *kk, double *c, uint64_t *pen, int32_t *deg, int V) {
+                           uint64_t *S, int32_t *kk, double *c, uint64_t *pen, int32_t *deg, int V, int voff) {
     const int n_live = scalars[0];
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
-        const int i = old_to_new[v];
+        const int i = old_to_new[voff + v];
         const uint64_t s = (i < n_live) ? S_rel[i] : 0ull;
-        const int k = csize[label[v]];
+        const int k = csize[label[voff + v]];
         // Wasserman-Faust closeness exactly as NetworkX evaluates it:
         // ((k-1)/S) * ((k-1)/(V-1)), binary64 RN, 0 if S == 0 or V <= 1.
         double cv = 0.0;
@@ -191,31 +201,75 @@ inline int nbits(uint64_t x) {
 
 }  // namespace
 
-void closeness(hm_ctx *ctx, Graph &G) {
+void closeness(hm_ctx *ctx, Graph &G) { closeness_multi(ctx, std::vector<Graph *>{&G}); }
+
+// Psi for several graphs in one fused pass over their disjoint union (each
+// graph is its own set of components; the MS-BFS batches all of them
+// together, so the per-level costs are shared).  Results are per graph.
+void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     cudaStream_t s = ctx->stream;
-    const int V = G.V;
-    HM_REQUIRE(V < (1 << 26), HM_ERANGE, "hm_closeness supports V < 2^26 (packed arc format)");
+    HM_REQUIRE(!gs.empty(), HM_EINVAL, "no graphs");
+    int64_t Vu64 = 0, nnz_u = 0;
+    for (Graph *g : gs) {
+        Vu64 += g->V;
+        nnz_u += g->nnz;
+    }
+    HM_REQUIRE(Vu64 < (1 << 26), HM_ERANGE, "hm_closeness supports sum V < 2^26 (packed arc format)");
+    HM_REQUIRE(nnz_u < (int64_t)INT32_MAX, HM_ERANGE, "union of graphs too large for an int32 CSR");
+    const int V = (int)Vu64;
     const int W = ctx->params.bfs_words;
     const unsigned gb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
     const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
     const int end_bit = 32 + nbits((uint64_t)V);
 
     // per-graph outputs
-    if (!G.S.p || G.S.bytes < (size_t)V * 8) {
-        G.S.alloc((size_t)V * 8, s);
-        G.k.alloc((size_t)V * 4, s);
-        G.c.alloc((size_t)V * 8, s);
-        G.pen.alloc((size_t)V * 8, s);
-        G.deg.alloc((size_t)V * 4, s);
-        G.ch.alloc((size_t)((V + 31) / 32) * 4 + 8 + 8, s);   // bitmap + mu + count
+    for (Graph *g : gs) {
+        const size_t Vg = (size_t)g->V;
+        if (!g->S.p || g->S.bytes < Vg * 8) {
+            g->S.alloc(Vg * 8, s);
+            g->k.alloc(Vg * 4, s);
+            g->c.alloc(Vg * 8, s);
+            g->pen.alloc(Vg * 8, s);
+            g->deg.alloc(Vg * 4, s);
+            g->ch.alloc(((Vg + 31) / 32) * 4 + 8 + 8, s);   // bitmap + mu + count
+        }
     }
+    // union CSR (a single graph is used in place)
+    Buf rp_ub, col_ub;
+    const int32_t *rp_u = gs[0]->row_ptr.as<int32_t>();
+    const int32_t *col_u = gs[0]->col.as<int32_t>();
+    std::vector<int> voff(gs.size(), 0);
+    if (gs.size() > 1) {
+        rp_ub.alloc((size_t)(V + 1) * 4, s);
+        col_ub.alloc((size_t)(nnz_u > 0 ? nnz_u : 1) * 4, s);
+        int vo = 0;
+        int64_t ao = 0;
+        for (size_t i = 0; i < gs.size(); ++i) {
+            voff[i] = vo;
+            const int64_t n = (int64_t)gs[i]->V + 1 > gs[i]->nnz ? (int64_t)gs[i]->V + 1 : gs[i]->nnz;
+            k_union_copy<<<grid_for(n, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(
+                gs[i]->row_ptr.as<int32_t>(), gs[i]->col.as<int32_t>(), gs[i]->V, gs[i]->nnz, vo, ao,
+                rp_ub.as<int32_t>(), col_ub.as<int32_t>());
+            vo += gs[i]->V;
+            ao += gs[i]->nnz;
+        }
+        check_launch("k_union_copy");
+        count_launch(ctx, (int)gs.size());
+        rp_u = rp_ub.as<int32_t>();
+        col_u = col_ub.as<int32_t>();
+    }
+    struct {
+        int V;
+        int64_t nnz;
+        const int32_t *rp, *col;
+    } U{V, nnz_u, rp_u, col_u};
 
     Buf parent((size_t)V * 4, s), label((size_t)V * 4, s), csize((size_t)V * 4, s);
     Buf key1((size_t)V * 8, s), key2((size_t)V * 8, s);
     Buf size_s((size_t)V * 4, s), cstart((size_t)V * 4, s), rank((size_t)V * 4, s);
     Buf n2o((size_t)V * 4, s), o2n((size_t)V * 4, s), ndeg((size_t)(V + 1) * 4, s);
     Buf nrp((size_t)(V + 1) * 4, s), cinfo((size_t)V * 8, s);
-    Buf ncol((size_t)(G.nnz > 0 ? G.nnz : 1) * 4, s), heavy((size_t)V * 4, s);
+    Buf ncol((size_t)(U.nnz > 0 ? U.nnz : 1) * 4, s), heavy((size_t)V * 4, s);
     Buf scal(64, s);
     int32_t *scalars = scal.as<int32_t>();
     HM_CUDA(cudaMemsetAsync(scal.p, 0, 64, s));
@@ -223,7 +277,7 @@ void closeness(hm_ctx *ctx, Graph &G) {
 
     // 1. connected components
     k_iota<<<gb, TB, 0, s>>>(parent.as<int32_t>(), V);
-    k_cc_union<<<gw, TB, 0, s>>>(G.row_ptr.as<int32_t>(), G.col.as<int32_t>(), parent.as<int32_t>(), V);
+    k_cc_union<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
     k_cc_compress<<<gb, TB, 0, s>>>(parent.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(), V);
     check_launch("cc");
     count_launch(ctx, 3);
@@ -250,7 +304,7 @@ void closeness(hm_ctx *ctx, Graph &G) {
         tbs = tb;
         HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tbs, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
                                                end_bit, s));
-        k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), G.row_ptr.as<int32_t>(), size_s.as<int32_t>(),
+        k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), U.rp, size_s.as<int32_t>(),
                                 cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
                                 ndeg.as<int32_t>(), cinfo.as<int2>(), V);
         tbs = tb;
@@ -259,7 +313,7 @@ void closeness(hm_ctx *ctx, Graph &G) {
         count_launch(ctx, 4 + 3 * 4 + 2);   // our kernels + CUB passes (approximate)
     }
     // 3. relabelled CSR + heavy list
-    k_relabel_cols<<<gw, TB, 0, s>>>(G.row_ptr.as<int32_t>(), G.col.as<int32_t>(), nrp.as<int32_t>(),
+    k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
                                      n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
                                      heavy.as<int32_t>(), scalars, ctx->params.bfs_heavy, V);
     check_launch("k_relabel_cols");
@@ -329,26 +383,30 @@ void closeness(hm_ctx *ctx, Graph &G) {
     count_launch(ctx);
     ctx->stats.bfs_launches += 1;
 
-    // 5. finalize
-    k_finalize<<<gb, TB, 0, s>>>(o2n.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(),
-                                 G.row_ptr.as<int32_t>(), Srel.as<uint64_t>(), scalars, G.S.as<uint64_t>(),
-                                 G.k.as<int32_t>(), G.c.as<double>(), G.pen.as<uint64_t>(),
-                                 G.deg.as<int32_t>(), V);
-    check_launch("k_finalize");
-    count_launch(ctx);
+    for (size_t gi = 0; gi < gs.size(); ++gi) {
+        Graph &G = *gs[gi];
+        const int Vg = G.V;
+        // 5. finalize (the graph's own V for closeness and the n-penalty)
+        k_finalize<<<grid_for(Vg, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(
+            o2n.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(), G.row_ptr.as<int32_t>(),
+            Srel.as<uint64_t>(), scalars, G.S.as<uint64_t>(), G.k.as<int32_t>(), G.c.as<double>(),
+            G.pen.as<uint64_t>(), G.deg.as<int32_t>(), Vg, voff[gi]);
+        check_launch("k_finalize");
+        count_launch(ctx);
 
-    // 6. mean closeness (exact) and CC nodes
-    uint32_t *chbm = G.ch.as<uint32_t>();
-    const size_t nbw = (size_t)(V + 31) / 32;
-    double *d_mu = reinterpret_cast<double *>(reinterpret_cast<char *>(chbm) + ((nbw * 4 + 7) / 8) * 8);
-    int32_t *d_cnt = reinterpret_cast<int32_t *>(d_mu + 1);
-    exact_mean(ctx, G.c.as<double>(), V, nullptr, d_mu, nullptr);
-    HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
-    k_cc_bitmap<<<grid_for((int64_t)V, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(G.c.as<double>(), d_mu, chbm,
-                                                                                   d_cnt, V);
-    check_launch("k_cc_bitmap");
-    count_launch(ctx);
-    G.has_results = true;
+        // 6. mean closeness (exact) and CC nodes
+        uint32_t *chbm = G.ch.as<uint32_t>();
+        const size_t nbw = (size_t)(Vg + 31) / 32;
+        double *d_mu = reinterpret_cast<double *>(reinterpret_cast<char *>(chbm) + ((nbw * 4 + 7) / 8) * 8);
+        int32_t *d_cnt = reinterpret_cast<int32_t *>(d_mu + 1);
+        exact_mean(ctx, G.c.as<double>(), Vg, nullptr, d_mu, nullptr);
+        HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
+        k_cc_bitmap<<<grid_for((int64_t)Vg, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(G.c.as<double>(), d_mu,
+                                                                                        chbm, d_cnt, Vg);
+        check_launch("k_cc_bitmap");
+        count_launch(ctx);
+        G.has_results = true;
+    }
 }
 
 }  // namespace hm

@@ -139,6 +139,7 @@ void build_csr(hm_ctx *ctx, int32_t V, const int32_t *edges_host_or_dev, int64_t
                int64_t *dropped);
 void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, Graph &out);
 void closeness(hm_ctx *ctx, Graph &G);
+void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs);
 // exact (correctly rounded) sum of masked non-negative doubles, then mean = sum / count;
 // result written to device double *d_mean (count taken from mask popcount or n)
 void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask_or_null,
@@ -149,5 +150,8 @@ void closeness_desc_keys(hm_ctx *ctx, const double *d_c, int32_t V, uint64_t *d_
 void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_ids_out);
 void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t K,
              int32_t *ids_out, int32_t *count_out);
+// Jaccard, precision, recall, F1, |est|, |gt|, |est ∩ gt| of two id lists (device)
+void set_metrics(hm_ctx *ctx, int32_t V, const int32_t *d_est, int64_t n_est, const int32_t *d_gt,
+                 int64_t n_gt, double *d_out7, int32_t *d_bad);
 
 }  // namespace hm

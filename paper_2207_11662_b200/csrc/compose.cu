@@ -148,7 +148,105 @@ __global__ void k_cc1_keys(LayerPtrs L, int V, const uint32_t *R, const int32_t 
     }
 }
 
+// CC2 with the "above-average" selection: Eq. 1 on estSumDist,
+// score = (V-1) / est in binary64 (est > 0 whenever V > 1).
+__global__ void k_cc2_scores(LayerPtrs L, int V, double *score) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        uint64_t e = L.pen[0][v];
+        for (int i = 1; i < L.r; ++i) e = max(e, L.pen[i][v]);
+        score[v] = e > 0 ? __ddiv_rn((double)(V - 1), (double)e) : 0.0;
+    }
+}
+
+// members: score > mean (strict, Z4); key 0 for members (ranked by id), ~0 otherwise
+__global__ void k_above_keys(const double *score, const double *mu, int V, uint64_t *key, int32_t *count) {
+    const int lane = threadIdx.x & 31;
+    const double m = *mu;
+    for (int64_t vb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31LL; vb < V;
+         vb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vb + lane;
+        const bool in = v < V && score[v] > m;
+        if (v < V) key[v] = in ? 0ull : ~0ull;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (lane == 0 && b) atomicAdd(count, __popc(b));
+    }
+}
+
+// id list -> membership bitmap (duplicates collapse: set semantics); an id
+// outside [0, V) sets *bad
+__global__ void k_ids_to_bitmap(const int32_t *ids, int64_t n, int V, uint32_t *bm, int32_t *bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ids[i];
+        if (v < 0 || v >= V) {
+            *bad = 1;
+            continue;
+        }
+        atomicOr(bm + (v >> 5), 1u << (v & 31));
+    }
+}
+
+// |A|, |B|, |A ∩ B| of two vertex bitmaps, then Jaccard / precision / recall /
+// F1 (PAPER.md:372; empty-set conventions SPEC.md:370, :379) in one thread.
+__global__ void k_set_counts(const uint32_t *a, const uint32_t *b, int nw, unsigned long long *cnt) {
+    unsigned long long ca = 0, cb = 0, cab = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
+        ca += __popc(a[i]);
+        cb += __popc(b[i]);
+        cab += __popc(a[i] & b[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ca += __shfl_xor_sync(0xffffffffu, ca, o);
+        cb += __shfl_xor_sync(0xffffffffu, cb, o);
+        cab += __shfl_xor_sync(0xffffffffu, cab, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(cnt + 0, ca);
+        atomicAdd(cnt + 1, cb);
+        atomicAdd(cnt + 2, cab);
+    }
+}
+
+__global__ void k_set_metrics(const unsigned long long *cnt, double *out) {
+    if (threadIdx.x != 0) return;
+    const double na = (double)cnt[0], nb = (double)cnt[1], nab = (double)cnt[2];
+    const double uni = na + nb - nab;
+    const double jac = uni > 0 ? nab / uni : 1.0;
+    const double p = na > 0 ? nab / na : (nb == 0 ? 1.0 : 0.0);
+    const double r = nb > 0 ? nab / nb : 1.0;
+    const double f = (p + r) > 0 ? 2.0 * p * r / (p + r) : 0.0;
+    out[0] = jac;
+    out[1] = p;
+    out[2] = r;
+    out[3] = f;
+    out[4] = na;
+    out[5] = nb;
+    out[6] = nab;
+}
+
 }  // namespace
+
+void set_metrics(hm_ctx *ctx, int32_t V, const int32_t *d_est, int64_t n_est, const int32_t *d_gt,
+                 int64_t n_gt, double *d_out7, int32_t *d_bad) {
+    cudaStream_t s = ctx->stream;
+    const int nw = (V + 31) / 32;
+    Buf bm((size_t)nw * 8, s), cnt(32, s);
+    HM_CUDA(cudaMemsetAsync(bm.p, 0, bm.bytes, s));
+    HM_CUDA(cudaMemsetAsync(cnt.p, 0, 32, s));
+    uint32_t *a = bm.as<uint32_t>(), *b = a + nw;
+    if (n_est > 0) {
+        k_ids_to_bitmap<<<grid_for(n_est, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(d_est, n_est, V, a, d_bad);
+        count_launch(ctx);
+    }
+    if (n_gt > 0) {
+        k_ids_to_bitmap<<<grid_for(n_gt, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(d_gt, n_gt, V, b, d_bad);
+        count_launch(ctx);
+    }
+    k_set_counts<<<grid_for(nw, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(a, b, nw,
+                                                                           cnt.as<unsigned long long>());
+    k_set_metrics<<<1, 32, 0, s>>>(cnt.as<unsigned long long>(), d_out7);
+    check_launch("set_metrics");
+    count_launch(ctx, 2);
+}
 
 void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t K, int32_t *ids_out,
              int32_t *count_out) {
@@ -179,11 +277,19 @@ void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t
         count_launch(ctx);
         topk(ctx, keys.as<uint64_t>(), V, K, ids.as<int32_t>());
         if (count_out) *count_out = K;
-    } else if (heuristic == HM_NAIVE || heuristic == HM_CC1) {
+    } else if (heuristic == HM_NAIVE || heuristic == HM_CC1 || heuristic == HM_CC2_AVG) {
         if (heuristic == HM_NAIVE) {
             k_naive_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>(), cnt.as<int32_t>());
             check_launch("k_naive_keys");
             count_launch(ctx);
+        } else if (heuristic == HM_CC2_AVG) {
+            Buf score((size_t)V * 8, s), mu(16, s);
+            k_cc2_scores<<<g, TB, 0, s>>>(L, V, score.as<double>());
+            exact_mean(ctx, score.as<double>(), V, nullptr, mu.as<double>(), nullptr);
+            k_above_keys<<<g, TB, 0, s>>>(score.as<double>(), mu.as<double>(), V, keys.as<uint64_t>(),
+                                         cnt.as<int32_t>());
+            check_launch("cc2 above-average");
+            count_launch(ctx, 2);
         } else {
             Buf mindeg((size_t)V * 4, s), ratio((size_t)V * r * 8, s), fin((size_t)V, s);
             Buf avgs((size_t)(r + 1) * 8, s), R((size_t)((V + 31) / 32) * 4, s);

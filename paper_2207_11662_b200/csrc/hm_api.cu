@@ -121,7 +121,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     HM_REQUIRE(name, HM_EINVAL, "null name");
     const std::string n(name);
     if (n == "bfs_words") {
-        HM_REQUIRE(value == 8 || value == 16 || value == 32, HM_EINVAL, "bfs_words must be 8, 16 or 32");
+        HM_REQUIRE(value == 8 || value == 16 || value == 32 || value == 64, HM_EINVAL,
+                   "bfs_words must be 8, 16, 32 or 64");
         ctx->params.bfs_words = (int)value;
     } else if (n == "bfs_heavy") {
         HM_REQUIRE(value >= 1, HM_EINVAL, "bfs_heavy must be >= 1");
@@ -237,6 +238,30 @@ hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reac
     HM_API_END(ctx)
 }
 
+hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(graph_ids && n >= 1, HM_EINVAL, "need n >= 1 graph ids");
+    std::set<int32_t> seen(graph_ids, graph_ids + n);
+    HM_REQUIRE((int32_t)seen.size() == n, HM_EINVAL, "repeated graph id");
+    std::vector<Graph *> gs;
+    for (int i = 0; i < n; ++i) gs.push_back(&graph(ctx, graph_ids[i]));
+    closeness_multi(ctx, gs);
+    HM_API_END(ctx)
+}
+
+hm_status hm_closeness_results(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach, double *closeness_out,
+                               uint64_t *pen_sum) {
+    HM_API_BEGIN(ctx)
+    Graph &G = graph(ctx, g);
+    HM_REQUIRE(G.has_results, HM_ESTATE, "hm_closeness_results before hm_closeness");
+    const size_t V = (size_t)G.V;
+    copy_out(ctx, dist_sum, G.S.p, V * 8);
+    copy_out(ctx, reach, G.k.p, V * 4);
+    copy_out(ctx, closeness_out, G.c.p, V * 8);
+    copy_out(ctx, pen_sum, G.pen.p, V * 8);
+    HM_API_END(ctx)
+}
+
 hm_status hm_cc_nodes(hm_ctx *ctx, int32_t g, uint32_t *bitmap, int32_t *count, double *mean) {
     HM_API_BEGIN(ctx)
     Graph &G = graph(ctx, g);
@@ -279,14 +304,45 @@ hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, i
                      int32_t *ids_out, int32_t *count_out) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(layer_ids && ids_out, HM_EINVAL, "null argument");
-    HM_REQUIRE(heuristic == HM_NAIVE || heuristic == HM_CC1 || heuristic == HM_CC2, HM_EINVAL,
-               "unknown heuristic");
+    HM_REQUIRE(heuristic == HM_NAIVE || heuristic == HM_CC1 || heuristic == HM_CC2 ||
+                   heuristic == HM_CC2_AVG,
+               HM_EINVAL, "unknown heuristic");
     HM_REQUIRE(r >= 2 && r <= 8, HM_EINVAL, "compose needs 2 <= r <= 8");
     std::set<int32_t> seen(layer_ids, layer_ids + r);
     HM_REQUIRE((int32_t)seen.size() == r, HM_EINVAL, "repeated graph id");
     std::vector<Graph *> gs;
     for (int i = 0; i < r; ++i) gs.push_back(&graph(ctx, layer_ids[i]));
     compose(ctx, heuristic, gs, K, ids_out, count_out);
+    HM_API_END(ctx)
+}
+
+hm_status hm_set_metrics(hm_ctx *ctx, int32_t V, const int32_t *est_ids, int64_t n_est,
+                         const int32_t *gt_ids, int64_t n_gt, double *out) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(out && V > 0 && n_est >= 0 && n_gt >= 0, HM_EINVAL, "bad argument");
+    HM_REQUIRE((n_est == 0 || est_ids) && (n_gt == 0 || gt_ids), HM_EINVAL, "null id list");
+    cudaStream_t s = ctx->stream;
+    // host id lists are staged to the device; device ones are read in place
+    Buf stage((size_t)(n_est + n_gt) * 4 + 4, s), res(7 * 8 + 8, s);
+    const int32_t *de = est_ids, *dg = gt_ids;
+    if (n_est && !is_device_ptr(est_ids)) {
+        HM_CUDA(cudaMemcpyAsync(stage.p, est_ids, (size_t)n_est * 4, cudaMemcpyHostToDevice, s));
+        de = stage.as<int32_t>();
+    }
+    if (n_gt && !is_device_ptr(gt_ids)) {
+        HM_CUDA(cudaMemcpyAsync(stage.as<int32_t>() + n_est, gt_ids, (size_t)n_gt * 4, cudaMemcpyHostToDevice, s));
+        dg = stage.as<int32_t>() + n_est;
+    }
+    HM_CUDA(cudaMemsetAsync(res.p, 0, res.bytes, s));
+    int32_t *d_bad = reinterpret_cast<int32_t *>(res.as<double>() + 7);
+    set_metrics(ctx, V, de, n_est, dg, n_gt, res.as<double>(), d_bad);
+    double h[8];
+    HM_CUDA(cudaMemcpyAsync(h, res.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    int32_t bad;
+    memcpy(&bad, &h[7], 4);
+    HM_REQUIRE(!bad, HM_ERANGE, "vertex id outside [0, V)");
+    memcpy(out, h, 7 * sizeof(double));
     HM_API_END(ctx)
 }
 

@@ -441,6 +441,7 @@ int launch_msbfs(int W, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaSt
         case 8: kern = (const void *)msbfs_kernel<8>; break;
         case 16: kern = (const void *)msbfs_kernel<16>; break;
         case 32: kern = (const void *)msbfs_kernel<32>; break;
+        case 64: kern = (const void *)msbfs_kernel<64>; break;
         default: return -1;
     }
     const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 * 2 : 0;

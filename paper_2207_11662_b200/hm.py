@@ -13,9 +13,9 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import HM_CC1, HM_CC2, HM_NAIVE  # noqa: F401
+from ._lib import HM_CC1, HM_CC2, HM_CC2_AVG, HM_NAIVE  # noqa: F401
 
-HEURISTICS = {"naive": HM_NAIVE, "cc1": HM_CC1, "cc2": HM_CC2}
+HEURISTICS = {"naive": HM_NAIVE, "cc1": HM_CC1, "cc2": HM_CC2, "cc2_avg": HM_CC2_AVG}
 
 
 class HmError(RuntimeError):
@@ -173,6 +173,30 @@ class Context:
                                         _ptr(res.get("c")), _ptr(res.get("pen"))))
         return res
 
+    def closeness_multi(self, gids):
+        """Closeness of several graphs in one fused pass (results cached per graph)."""
+        arr = (ctypes.c_int32 * len(gids))(*gids)
+        self._check(self.L.hm_closeness_multi(self.h, arr, len(gids)))
+
+    def closeness_results(self, g, out=None, want=("S", "k", "c", "pen")):
+        """Cached closeness results of graph g (numpy by default, or into ``out``)."""
+        V, _ = self.graph_info(g)
+        if out is None:
+            res = {}
+            if "S" in want:
+                res["S"] = np.zeros(V, np.uint64)
+            if "k" in want:
+                res["k"] = np.zeros(V, np.int32)
+            if "c" in want:
+                res["c"] = np.zeros(V, np.float64)
+            if "pen" in want:
+                res["pen"] = np.zeros(V, np.uint64)
+        else:
+            res = out
+        self._check(self.L.hm_closeness_results(self.h, int(g), _ptr(res.get("S")), _ptr(res.get("k")),
+                                                _ptr(res.get("c")), _ptr(res.get("pen"))))
+        return res
+
     def cc_nodes(self, g):
         """(sorted numpy array of CC nodes, count, mean closeness)."""
         V, _ = self.graph_info(g)
@@ -196,7 +220,7 @@ class Context:
 
     # -------------------------------------------------------- composition
     def compose(self, heuristic, ids, K, out=None):
-        """heuristic in {'cc1','cc2','naive'}.  Returns (ranked ids, |result set|)."""
+        """heuristic in {'cc1','cc2','cc2_avg','naive'}.  Returns (ranked ids, |result set|)."""
         h = HEURISTICS[heuristic] if isinstance(heuristic, str) else int(heuristic)
         arr = (ctypes.c_int32 * len(ids))(*ids)
         buf = np.zeros(K, np.int32) if out is None else out
@@ -206,3 +230,20 @@ class Context:
         if out is None:
             return buf[:min(K, n)], n
         return buf, n
+
+    # ------------------------------------------------------------ metrics
+    def set_metrics(self, V, est, gt):
+        """Accuracy of an estimated id list vs the ground truth:
+        dict jaccard, precision, recall, f1, n_est, n_gt, n_common."""
+        def arr(x):
+            if x is None or (not isinstance(x, np.ndarray) and hasattr(x, "data_ptr")):
+                return x
+            return np.ascontiguousarray(np.asarray(x, dtype=np.int32).reshape(-1))
+        est, gt = arr(est), arr(gt)
+        ne = 0 if est is None else int(est.shape[0])
+        ng = 0 if gt is None else int(gt.shape[0])
+        out = (ctypes.c_double * 7)()
+        self._check(self.L.hm_set_metrics(self.h, int(V), _ptr(est) if ne else None, ne,
+                                          _ptr(gt) if ng else None, ng, out))
+        keys = ("jaccard", "precision", "recall", "f1", "n_est", "n_gt", "n_common")
+        return {k: (float(v) if i < 4 else int(v)) for i, (k, v) in enumerate(zip(keys, out))}

@@ -106,7 +106,7 @@ def test_tuning_invariance(hm):
     V = 3000
     E = {tuple(e) for e in random_graph(V, 6 * V, seed=77, kind="rmat").tolist()}
     res = O.analyze(V, E)
-    for words in (8, 16, 32):
+    for words in (8, 16, 32, 64):
         for heavy in (4, 64, 100000):
             for bps in (0, 1):
                 with hm() as ctx:
@@ -190,7 +190,23 @@ def run_pipeline_and_compare(ctx, h, check_layers=True):
         idsn, nn = ctx.compose("naive", list(T), K)
         rn, nrn, _ = O.naive(rs, K)
         assert nn == nrn and idsn.tolist() == rn
+        # CC2 "above average" selection: the whole set, ids ascending
+        avg = sorted(O.cc2_above_average(rs))
+        idsa, na = ctx.compose("cc2_avg", list(T), V)
+        assert na == len(avg) and idsa.tolist() == avg
+        # accuracy metrics of each estimate against the GT top-K
+        gt = O.topk_closeness(ra["c"], K)
+        for est in (ids2.tolist(), ids1.tolist(), idsn.tolist(), avg):
+            m = ctx.set_metrics(V, est, gt)
+            p, r, f = O.prf1(est, gt)
+            assert (m["jaccard"], m["precision"], m["recall"], m["f1"]) == (O.jaccard(est, gt), p, r, f)
         ctx.free_graph(g)
+        # OR aggregation, edge set exact
+        go = ctx.or_aggregate(list(T))
+        rp, col = ctx.graph_csr(go)
+        src = np.repeat(np.arange(V), np.diff(rp))
+        assert {(int(a), int(b)) for a, b in zip(src, col) if a < b} == O.or_aggregate([Es[i] for i in T])
+        ctx.free_graph(go)
 
 
 @pytest.mark.parametrize("name,V", homln_cases(), ids=[f"{n}@{v or 'full'}" for n, v in homln_cases()])
@@ -217,6 +233,33 @@ def test_cc1_golden_on_gpu(hm):
         assert ctx.topk_closeness(a, 3).tolist() == g["GT_top3"]
 
 
+def test_set_metrics_edge_cases(hm):
+    """Jaccard / P / R / F1 incl. empty sets, duplicates, device
+    lists and out-of-range ids (SPEC.md:370, :379 conventions)."""
+    import torch
+    from paper_2207_11662_b200 import HmError
+    rng = random.Random(5)
+    cases = [([], []), ([], [1, 2]), ([3], []), ([1, 1, 2], [2, 2]), (list(range(100)), list(range(50, 150)))]
+    for _ in range(30):
+        V = rng.choice([1, 31, 32, 33, 1000, 70000])
+        cases.append(([rng.randrange(V) for _ in range(rng.randrange(0, 300))],
+                      [rng.randrange(V) for _ in range(rng.randrange(0, 300))]))
+    with hm() as ctx:
+        for a, b in cases:
+            V = max([0] + a + b) + 1
+            m = ctx.set_metrics(V, a, b)
+            p, r, f = O.prf1(a, b)
+            assert (m["jaccard"], m["precision"], m["recall"], m["f1"]) == (O.jaccard(a, b), p, r, f), (a, b)
+            assert (m["n_est"], m["n_gt"], m["n_common"]) == (len(set(a)), len(set(b)), len(set(a) & set(b)))
+        a = torch.tensor([0, 5, 9], dtype=torch.int32, device="cuda")
+        b = torch.tensor([5, 9, 11], dtype=torch.int32, device="cuda")
+        assert ctx.set_metrics(12, a, b)["jaccard"] == 0.5
+        with pytest.raises(HmError, match="HM_ERANGE"):
+            ctx.set_metrics(10, [0, 10], [1])
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.set_metrics(0, [], [])
+
+
 def test_device_tensors_roundtrip(hm):
     import torch
     h = build_config("C5", V=2048)
@@ -236,3 +279,27 @@ def test_device_tensors_roundtrip(hm):
         ctx.topk_closeness(0, 10, out=ids)
         ctx.sync()
         assert ids.cpu().tolist() == O.topk_closeness(res["c"], 10)
+
+
+@pytest.mark.parametrize("name,V", [("C3", 1024), ("C5", 4096), ("C4", 2048)])
+def test_closeness_multi_fused(hm, name, V):
+    """one fused pass over layers + AND graphs == separate passes == oracle."""
+    h = build_config(name, V=V)
+    Es = [set(map(tuple, L.tolist())) for L in h.layers]
+    with hm() as ctx:
+        ids, _ = ctx.load_layers(h.V, h.layers)
+        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        gids = list(ids) + ands
+        ctx.closeness_multi(gids)
+        fused = {g: ctx.closeness_results(g) for g in gids}
+        fused_ch = {g: ctx.cc_nodes(g) for g in gids}
+        for g in gids:
+            sep = ctx.closeness(g)
+            for key in ("S", "k", "c", "pen"):
+                assert np.array_equal(fused[g][key], sep[key]), (g, key)
+            nodes, cnt, mu = ctx.cc_nodes(g)
+            assert np.array_equal(nodes, fused_ch[g][0]) and mu == fused_ch[g][2]
+        for i in ids:
+            check_psi(h.V, Es[i], fused[i])
+        for T, g in zip(h.subsets, ands):
+            check_psi(h.V, O.and_aggregate([Es[i] for i in T]), fused[g])

@@ -432,6 +432,27 @@ def test_tie_breaks():
     assert O.cc1(rs, 4)[1] == 0                    # CH empty on C_n (strict >)
 
 
+def test_cc2_above_average_pins():
+    """CC2 above-average pinned by hand and by reduction."""
+    # hand-worked: L1 = path 0-1-2 + isolated 3 (pen 7, 6, 7, 12), L2 = K4 (pen 3);
+    # est = (7, 6, 7, 12), score = 3/est = (.4286, .5, .4286, .25), mean .4018
+    L1 = {(0, 1), (1, 2)}
+    L2 = {(u, v) for u in range(4) for v in range(u + 1, 4)}
+    rs = [O.analyze(4, L1), O.analyze(4, L2)]
+    assert rs[0]["pen"] == [7, 6, 7, 12]
+    assert O.cc2_above_average(rs) == {0, 1, 2}
+    # identical connected layers: est = S, score = (V-1)/S = Eq. 1 closeness, so
+    # the set is the CC-node set CH of the layer itself (PAPER.md:186)
+    for seed in range(5):
+        V = 40
+        E = {tuple(e) for e in random_graph(V, 3 * V, seed=300 + seed, kind="er").tolist()} | path(V)
+        r = O.analyze(V, E)
+        assert O.cc2_above_average([r, r]) == r["CH"]
+    # path P3: scores (2/3, 1, 2/3), mean 7/9 -> {1}
+    r = O.analyze(3, path(3))
+    assert O.cc2_above_average([r, r]) == {1}
+
+
 def test_metrics_spec_examples():
     assert O.jaccard({1, 2, 3}, {2, 3, 4}) == 0.5
     assert O.jaccard(set(), set()) == 1.0
