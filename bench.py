@@ -394,7 +394,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--words", type=int, default=32)
+    ap.add_argument("--words", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -18,7 +18,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC",
     "-I", os.path.join(ROOT, "include"),
-]
+] + (["-DHM_MSBFS_PROF"] if os.environ.get("HM_MSBFS_PROF") else [])
 
 
 def sources():

@@ -312,10 +312,11 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
         check_launch("relabel");
         count_launch(ctx, 4 + 3 * 4 + 2);   // our kernels + CUB passes (approximate)
     }
-    // 3. relabelled CSR + heavy list
+    // 3. relabelled CSR + heavy list (rows heavier than the MS-BFS light path takes)
+    const int heavy_deg = ctx->params.bfs_heavy < BFS_MAX_LIGHT_DEG ? ctx->params.bfs_heavy : BFS_MAX_LIGHT_DEG;
     k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
                                      n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
-                                     heavy.as<int32_t>(), scalars, ctx->params.bfs_heavy, V);
+                                     heavy.as<int32_t>(), scalars, heavy_deg, V);
     check_launch("k_relabel_cols");
     count_launch(ctx);
 
@@ -343,7 +344,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     a.comp_start = cstart.as<int32_t>();
     a.scalars = scalars;
     a.heavy = heavy.as<int32_t>();
-    a.heavy_deg = ctx->params.bfs_heavy;
+    a.heavy_deg = heavy_deg;
     a.F[0] = F0.as<uint64_t>();
     a.F[1] = F1.as<uint64_t>();
     a.F[2] = F2.as<uint64_t>();
@@ -352,7 +353,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     a.done = bm + 4 * bmw;
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
-    a.chg_smem = (bmw * 4 * 2 <= 80 * 1024) ? 1 : 0;
+    a.chg_smem = (ctx->params.bfs_chg_smem && bmw * 4 * 2 <= 80 * 1024) ? 1 : 0;
     a.S = Srel.as<uint64_t>();
     a.flags = flags.as<int32_t>();
     a.counters = ctx->dstats.as<unsigned long long>();
@@ -370,7 +371,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
         HM_CUDA(cudaEventCreate(&e1));
         HM_CUDA(cudaEventRecord(e0, s));
     }
-    const int grid = launch_msbfs(W, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
+    const int grid = launch_msbfs(W, ctx->params.bfs_team, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
     if (grid < 0) {
         cudaGetLastError();
         throw Error(HM_ECUDA, "msbfs launch failed (" + std::to_string(grid) + ")");

@@ -83,9 +83,11 @@ struct Graph {
 };
 
 struct Params {
-    int bfs_words = 32;
+    int bfs_words = 64;
     int bfs_heavy = 256;
     int bfs_blocks_per_sm = 0;
+    int bfs_chg_smem = 1;
+    int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level
     int timing = 0;
     int bfs_dbg = 0;
 };

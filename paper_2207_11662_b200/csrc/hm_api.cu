@@ -130,6 +130,12 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_blocks_per_sm") {
         HM_REQUIRE(value >= 0, HM_EINVAL, "bfs_blocks_per_sm must be >= 0");
         ctx->params.bfs_blocks_per_sm = (int)value;
+    } else if (n == "bfs_team") {
+        HM_REQUIRE(value == 0 || value == 4 || value == 8 || value == 16 || value == 32, HM_EINVAL,
+                   "bfs_team must be 0 (default), 4, 8, 16 or 32 (and at most words/2)");
+        ctx->params.bfs_team = (int)value;
+    } else if (n == "bfs_chg_smem") {
+        ctx->params.bfs_chg_smem = value ? 1 : 0;
     } else if (n == "bfs_dbg") {
         ctx->params.bfs_dbg = (int)value;
     } else if (n == "timing") {

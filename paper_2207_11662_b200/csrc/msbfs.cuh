@@ -5,6 +5,9 @@
 
 namespace hm {
 
+// Rows of degree > min(heavy_deg, BFS_MAX_LIGHT_DEG) are processed by whole CTAs.
+constexpr int BFS_MAX_LIGHT_DEG = 1 << 30;
+
 // Device-resident description of one relabelled graph for the MS-BFS kernel.
 // Rows 0..n_live-1 are the non-isolated vertices, grouped by connected
 // component, components sorted by size descending (see closeness.cu).
@@ -24,13 +27,15 @@ struct BfsArgs {
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches
-    unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times
+    unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per
-// batch).  blocks_per_sm == 0 -> occupancy maximum.  Returns the grid size.
-int launch_msbfs(int W, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s);
+// batch).  Returns the grid size (< 0: no instantiation / launch failure).
+// TL = lanes per state row in the light path (0 = default: W/2, 16 at W = 64);
+// blocks_per_sm == 0 -> occupancy maximum.
+int launch_msbfs(int W, int TL, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s);
 
 }  // namespace hm

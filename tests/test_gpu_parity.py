@@ -75,9 +75,17 @@ def special_graphs():
 @pytest.mark.parametrize("name,V,E", special_graphs(), ids=[g[0] for g in special_graphs()])
 def test_psi_special(hm, name, V, E):
     E = {(min(u, v), max(u, v)) for u, v in E if u != v}
+    res = O.analyze(V, E)
+    # narrow batches (B = 512: several batches per component), other team widths and occupancies
+    for words, team, bps in ((8, 0, 0), (16, 4, 1), (64, 32, 0), (64, 16, 0)):
+        with hm() as ctx:
+            ctx.set_param("bfs_words", words)
+            ctx.set_param("bfs_team", team)
+            ctx.set_param("bfs_blocks_per_sm", bps)
+            check_psi(V, E, run_graph(ctx, V, E), res)
     with hm() as ctx:
         got = run_graph(ctx, V, E)
-        res = check_psi(V, E, got)
+        check_psi(V, E, got, res)
         nodes, cnt, mu = ctx.cc_nodes(0)
         assert set(nodes.tolist()) == res["CH"] and cnt == len(res["CH"])
         assert mu == res["mu"]
@@ -109,11 +117,13 @@ def test_tuning_invariance(hm):
     for words in (8, 16, 32, 64):
         for heavy in (4, 64, 100000):
             for bps in (0, 1):
-                with hm() as ctx:
-                    ctx.set_param("bfs_words", words)
-                    ctx.set_param("bfs_heavy", heavy)
-                    ctx.set_param("bfs_blocks_per_sm", bps)
-                    check_psi(V, E, run_graph(ctx, V, E), res)
+                for chg_smem in (0, 1):
+                    with hm() as ctx:
+                        ctx.set_param("bfs_words", words)
+                        ctx.set_param("bfs_heavy", heavy)
+                        ctx.set_param("bfs_blocks_per_sm", bps)
+                        ctx.set_param("bfs_chg_smem", chg_smem)
+                        check_psi(V, E, run_graph(ctx, V, E), res)
 
 
 def test_loader_canonicalises(hm):
