@@ -127,6 +127,7 @@ def run_ours(args, rank, world, local_rank):
     ctx = Context(dev)
     s = ctx.stream
     ctx.set_param("bfs_words", args.words)
+    ctx.set_param("bfs_hints", args.hints)
     ctx.set_param("timing", 1)
     host_layers = [torch.from_numpy(L).pin_memory() for L in h.layers]
     dev_layers = [t.to(f"cuda:{dev}") for t in host_layers]
@@ -265,8 +266,10 @@ def run_ours(args, rank, world, local_rank):
         Vl, Al = V * len(arcs), float(np.sum(arcs))
     model_bytes = levels_per_launch * (4 * (Vl + 1) + 4 * Al + 3 * Rb * Vl)
     achieved = model_bytes / (bfs_ms_avg / 1e3) / 1e9 if bfs_ms_avg > 0 else 0.0
+    traffic, traffic_src = measured_traffic(args)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-            "frac": achieved / peak_gbs, "traffic": None, "peak_source": peak_src,
+            "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": peak_src,
             "kernel": "msbfs_kernel", "bytes_model": "SURVEY 8(d) dense-level: L*(4(V+1)+4A+3RV)",
             "bytes_per_launch": model_bytes, "ms_per_launch": bfs_ms_avg,
             "levels_per_launch": levels_per_launch, "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9),
@@ -280,7 +283,7 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": h.name, "V": V, "layers": len(h.layers), "subsets": [list(t) for t in h.subsets],
                    "K": K, "recipe": h.recipe, "units_W": W_total, "units_per_graph": dict(zip(graph_names, units)),
-                   "bfs_words": args.words, "sources_per_batch": 64 * args.words,
+                   "bfs_words": args.words, "bfs_hints": args.hints, "sources_per_batch": 64 * args.words,
                    "l2": "flushed (256 MiB write) before each timed step", "parallelism": f"replicas{world}"},
         "s_per_homln": ms_per_step / 1e3,
         "e2e": e2e, "roofline": roof, "clocks": clocks, "gpu_launches": int(round(launches_per_step)),
@@ -326,6 +329,21 @@ def oracle_sample(V, E, seconds, threads, seed=0, graph=None):
             break
         n = int(min(V, max(n * 2, n * (seconds * 0.5 - t_total) / max(dt, 1e-3))))
     return u_total, t_total, s_total
+
+
+def measured_traffic(args):
+    """roofline.traffic: DRAM bytes per MS-BFS launch from the committed ncu capture
+    (tools/ncu_traffic.py) when it was taken on this config, batch width and L2 policy."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_msbfs_traffic.json")))
+    for f in reversed(files):
+        try:
+            t = json.load(open(f))
+        except Exception:
+            continue
+        if t.get("config") == args.config and t.get("bfs_words") == args.words and t.get("bfs_hints") == args.hints:
+            return t["dram_bytes_per_launch"], os.path.relpath(f, ROOT)
+    return None, None
 
 
 def cpu_baseline(h, seconds):
@@ -395,6 +413,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--words", type=int, default=64)
+    ap.add_argument("--hints", type=int, default=11, help="MS-BFS L2 eviction-priority bits (library bfs_hints)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -63,6 +63,9 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16, 32 or 64; sources per batch = 64*words)
  *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (0 = occupancy maximum)
+ *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
+ *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
+ *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16 or 8)
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)
  *   "bfs_chg_smem": 1 (default) stages the per-level change bitmaps in shared memory, 0 reads them via L1
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)

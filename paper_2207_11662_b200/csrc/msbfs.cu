@@ -140,15 +140,44 @@ __device__ __forceinline__ void or_row(ulonglong2 (&r)[VEC], const ulonglong2 (&
         r[q].y |= x[q].y;
     }
 }
-template <int W, int TL, int VEC>
-__device__ __forceinline__ void ld_row(ulonglong2 (&r)[VEC], const uint64_t *F, int v, int l) {
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) r[q] = ld2(F + (size_t)v * W + 2 * (q * TL + l));
+// L2 cache-policy variants (createpolicy + .L2::cache_hint); pol == 0 -> plain access
+__device__ __forceinline__ ulonglong2 ld2p(const uint64_t *p, uint64_t pol) {
+    if (!pol) return ld2(p);
+    ulonglong2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st2p(uint64_t *p, ulonglong2 v, uint64_t pol) {
+    if (!pol) {
+        st2(p, v);
+        return;
+    }
+    asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(p), "l"(v.x), "l"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 template <int W, int TL, int VEC>
-__device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglong2 (&r)[VEC]) {
+__device__ __forceinline__ void ld_row(ulonglong2 (&r)[VEC], const uint64_t *F, int v, int l, uint64_t pol = 0) {
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) st2(F + (size_t)v * W + 2 * (q * TL + l), r[q]);
+    for (int q = 0; q < VEC; ++q) r[q] = ld2p(F + (size_t)v * W + 2 * (q * TL + l), pol);
+}
+template <int W, int TL, int VEC>
+__device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglong2 (&r)[VEC], uint64_t pol = 0) {
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) st2p(F + (size_t)v * W + 2 * (q * TL + l), r[q], pol);
 }
 
 // W words per row; TL lanes per light row
@@ -188,6 +217,12 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
     int32_t *su = sm.su[wib];
     uint8_t *sr = sm.sr[wib];
     int16_t *seg = sm.seg[wib];
+    // L2 eviction-priority policies (a.hints bits): gathered F_{d-1} rows, own F_{d-2} rows, F_d stores
+    // (bit 4: use the hinted instructions with evict_normal where no other policy is set)
+    const uint64_t pol_d = (a.hints & 16) ? policy_evict_normal() : 0ull;
+    const uint64_t pol_c = (a.hints & 1) ? policy_evict_last() : pol_d;
+    const uint64_t pol_p = (a.hints & 2) ? policy_evict_first() : pol_d;
+    const uint64_t pol_n = (a.hints & 4) ? policy_evict_last() : (a.hints & 8) ? policy_evict_first() : pol_d;
     Prof pf;
     PROF_INIT(pf);
 
@@ -245,7 +280,7 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
             if (gtid == 0) a.flags[(d + 1) % 3] = 0;
             // stage the two previous change bitmaps in shared memory
             const uint32_t *chp_s = chp, *chpp_s = chpp;
-            if (threadIdx.x == 0) sm.next = (int)(((int64_t)blockIdx.x * ngroups) / gridDim.x);
+            if (threadIdx.x == 0) sm.next = (int)(((int64_t)blockIdx.x * (ngroups << a.unit_shift)) / gridDim.x);
             if (a.chg_smem) {
                 const int nw4 = (int)((ngroups + 3) >> 2);
                 uint4 *d0 = s_dyn;
@@ -328,29 +363,36 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
             }
             PROF_MARK(pf, 1);
 
-            // ---- light rows: one warp per 32-row group; each CTA owns a contiguous
-            // range of groups and its warps claim them dynamically (load balance)
-            const int64_t g_end = ((int64_t)(blockIdx.x + 1) * ngroups) / gridDim.x;
+            // ---- light rows: one warp per unit of 32 >> unit_shift rows of a 32-row group;
+            // each CTA owns a contiguous range of units and its warps claim them
+            // dynamically (smaller units: less end-of-level quantisation)
+            const int us = a.unit_shift;
+            const int ur = 32 >> us;                                    // rows per unit
+            const int64_t nunits = ngroups << us;
+            const int64_t u_end = ((int64_t)(blockIdx.x + 1) * nunits) / gridDim.x;
             for (;;) {
-                int64_t g = 0;
-                if (lane == 0) g = (int64_t)atomicAdd(&sm.next, 1);
-                g = __shfl_sync(FULL, g, 0);
-                if (g >= g_end) break;
+                int64_t un = 0;
+                if (lane == 0) un = (int64_t)atomicAdd(&sm.next, 1);
+                un = __shfl_sync(FULL, un, 0);
+                if (un >= u_end) break;
+                const int64_t g = un >> us;
+                const int q0 = (int)(un & ((1 << us) - 1)) * ur;           // first row of the unit in the group
                 const int r = (int)(g * 32 + lane);
                 const bool valid = r < hi;
+                const bool inunit = lane >= q0 && lane < q0 + ur;
                 const int rp = a.row_ptr[valid ? r : hi];
                 const int rlast = a.row_ptr[(int)(g * 32 + 32) < hi ? (int)(g * 32 + 32) : hi];
                 const uint32_t dword = a.done[g];
                 const int rnext = __shfl_down_sync(FULL, rp, 1);
                 const int rend = (lane == 31) ? rlast : rnext;
-                const bool act = valid && !((dword >> lane) & 1u) && (rend - rp) <= heavy_deg;
+                const bool act = valid && inunit && !((dword >> lane) & 1u) && (rend - rp) <= heavy_deg;
                 const unsigned amask = __ballot_sync(FULL, act);
                 PROF_MARK(pf, 2);
                 if (!amask) continue;                                    // warp-uniform
                 const uint32_t pword = chp_s[g], ppword = chpp_s[g];
                 uint32_t chg_bits = 0u, done_bits = 0u;
-                const int A0 = __shfl_sync(FULL, rp, 0);
-                const int A1 = rlast;
+                const int A0 = __shfl_sync(FULL, rp, q0);
+                const int A1 = __shfl_sync(FULL, rend, q0 + ur - 1);    // end of the unit's last row
                 int n = 0;
                 for (int a0 = A0; a0 < A1; a0 += 32 * SCAN_U) {
                     int xx[SCAN_U];
@@ -414,8 +456,8 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                         ulonglong2 vv[VEC], v2[VEC];
                         zero_row<VEC>(vv);
                         zero_row<VEC>(v2);
-                        if (has && ((pword >> ri) & 1u)) ld_row<W, TL, VEC>(vv, Fc, v, ltl);
-                        if (has && ((ppword >> ri) & 1u)) ld_row<W, TL, VEC>(v2, Fp, v, ltl);
+                        if (has && ((pword >> ri) & 1u)) ld_row<W, TL, VEC>(vv, Fc, v, ltl, pol_c);
+                        if (has && ((ppword >> ri) & 1u)) ld_row<W, TL, VEC>(v2, Fp, v, ltl, pol_p);
                         int Kv = 0;
                         uint64_t Sv = 0;
                         if (has && ltl == 0) {
@@ -431,7 +473,7 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
         #pragma unroll
                             for (int q = 0; q < GD; ++q) {
                                 zero_row<VEC>(x[q]);
-                                if (k0 + q < ke) ld_row<W, TL, VEC>(x[q], Fc, su[k0 + q], ltl);
+                                if (k0 + q < ke) ld_row<W, TL, VEC>(x[q], Fc, su[k0 + q], ltl, pol_c);
                             }
         #pragma unroll
                             for (int q = 0; q < GD; ++q) or_row<VEC>(acc, x[q]);
@@ -455,7 +497,7 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
                         for (int o = TL / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
                         if (cnt) {
                             or_row<VEC>(acc, f0);
-                            st_row<W, TL, VEC>(Fn, v, ltl, acc);
+                            st_row<W, TL, VEC>(Fn, v, ltl, acc, pol_n);
                             if (ltl == 0) {
                                 const int2 ci = comp_of(a, v, n_giant);
                                 int64_t nb = (int64_t)ci.y - base;

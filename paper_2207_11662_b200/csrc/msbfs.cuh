@@ -30,6 +30,9 @@ struct BfsArgs {
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
+    int unit_shift;
+    int hints;                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
+                                 // 4 F_d stores evict_last, 8 F_d stores evict_first              // light-path work unit = 32 >> unit_shift rows of a 32-row group
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per

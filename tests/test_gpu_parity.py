@@ -77,9 +77,10 @@ def test_psi_special(hm, name, V, E):
     E = {(min(u, v), max(u, v)) for u, v in E if u != v}
     res = O.analyze(V, E)
     # narrow batches (B = 512: several batches per component), other team widths and occupancies
-    for words, team, bps in ((8, 0, 0), (16, 4, 1), (64, 32, 0), (64, 16, 0)):
+    for words, team, bps, unit in ((8, 0, 0, 8), (16, 4, 1, 16), (64, 32, 0, 32), (64, 16, 0, 8)):
         with hm() as ctx:
             ctx.set_param("bfs_words", words)
+            ctx.set_param("bfs_unit", unit)
             ctx.set_param("bfs_team", team)
             ctx.set_param("bfs_blocks_per_sm", bps)
             check_psi(V, E, run_graph(ctx, V, E), res)
@@ -117,8 +118,9 @@ def test_tuning_invariance(hm):
     for words in (8, 16, 32, 64):
         for heavy in (4, 64, 100000):
             for bps in (0, 1):
-                for chg_smem in (0, 1):
+                for chg_smem, unit in ((0, 32), (1, 8)):
                     with hm() as ctx:
+                        ctx.set_param("bfs_unit", unit)
                         ctx.set_param("bfs_words", words)
                         ctx.set_param("bfs_heavy", heavy)
                         ctx.set_param("bfs_blocks_per_sm", bps)

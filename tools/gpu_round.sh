@@ -10,7 +10,8 @@ CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "ncu list rc=$?"
-P="python tools/prof_c5.py --graph 0"
+# full capture of the 4 MS-BFS launches of bench.py's setup pass (3 layers + AND of one HoMLN)
+P="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
 $P > gpurun_out/plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:msbfs -s 1 -c 1 -o gpurun_out/msbfs_full -f $P > gpurun_out/ncu_full.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:msbfs -c 4 -o gpurun_out/msbfs_full -f $P > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"

@@ -8,8 +8,12 @@ want = ["Duration", "DRAM Throughput", "L2 Cache Throughput", "L1/TEX Cache Thro
         "Executed Ipc Active", "L1/TEX Hit Rate", "L2 Hit Rate", "Memory Throughput", "Warp Cycles Per Issued Instruction",
         "Executed Instructions", "Avg. Active Threads Per Warp", "Registers Per Thread", "Achieved Occupancy",
         "Eligible Warps Per Scheduler", "No Eligible"]
+ids = [dict(zip(hdr, row)).get("ID") for row in r[1:]]
+first = ids[0] if ids else None
 for row in r[1:]:
     d = dict(zip(hdr, row))
+    if d.get("ID") != first:          # first captured launch only
+        continue
     if d.get("Metric Name") in want:
         print(f"  {d['Metric Name']:<40} {d['Metric Value']:>16} {d['Metric Unit']}")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -23,7 +27,12 @@ for k in ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "
 sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(sass)))
 hdr = rows[1]
-data = [dict(zip(hdr, x)) for x in rows[2:] if len(x) == len(hdr)]
+data = []
+for x in rows[2:]:                    # first kernel's section only
+    if x and x[0] == "Kernel Name":
+        break
+    if len(x) == len(hdr) and x[0] != hdr[0]:
+        data.append(dict(zip(hdr, x)))
 f = lambda x: float(x) if x not in ("", None) else 0.0
 tot = sum(f(d["Warp Stall Sampling (All Samples)"]) for d in data) or 1
 stalls = [c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
