@@ -373,7 +373,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
         HM_CUDA(cudaEventCreate(&e1));
         HM_CUDA(cudaEventRecord(e0, s));
     }
-    const int grid = launch_msbfs(W, ctx->params.bfs_team, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
+    const int grid = launch_msbfs(W, ctx->params.bfs_team, ctx->params.bfs_gd, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
     if (grid < 0) {
         cudaGetLastError();
         throw Error(HM_ECUDA, "msbfs launch failed (" + std::to_string(grid) + ")");

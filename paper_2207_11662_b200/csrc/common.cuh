@@ -89,6 +89,7 @@ struct Params {
     int bfs_chg_smem = 1;
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
     int bfs_unit = 32;         // MS-BFS light-path rows per work unit (32, 16, 8)
+    int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level
     int timing = 0;
     int bfs_dbg = 0;

@@ -128,7 +128,7 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value >= 1, HM_EINVAL, "bfs_heavy must be >= 1");
         ctx->params.bfs_heavy = (int)value;
     } else if (n == "bfs_blocks_per_sm") {
-        HM_REQUIRE(value >= 0, HM_EINVAL, "bfs_blocks_per_sm must be >= 0");
+        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_blocks_per_sm must be 0 (= 2), 1 or 2");
         ctx->params.bfs_blocks_per_sm = (int)value;
     } else if (n == "bfs_hints") {
         HM_REQUIRE(value >= 0 && value <= 31, HM_EINVAL, "bfs_hints must be in [0, 31]");
@@ -136,6 +136,9 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_unit") {
         HM_REQUIRE(value == 8 || value == 16 || value == 32, HM_EINVAL, "bfs_unit must be 8, 16 or 32");
         ctx->params.bfs_unit = (int)value;
+    } else if (n == "bfs_gd") {
+        HM_REQUIRE(value == 0 || value == 2 || value == 4 || value == 8, HM_EINVAL, "bfs_gd must be 0, 2, 4 or 8");
+        ctx->params.bfs_gd = (int)value;
     } else if (n == "bfs_team") {
         HM_REQUIRE(value == 0 || value == 4 || value == 8 || value == 16 || value == 32, HM_EINVAL,
                    "bfs_team must be 0 (default), 4, 8, 16 or 32 (and at most words/2)");

@@ -180,16 +180,15 @@ __device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglon
     for (int q = 0; q < VEC; ++q) st2p(F + (size_t)v * W + 2 * (q * TL + l), r[q], pol);
 }
 
-// W words per row; TL lanes per light row
-template <int W, int TL>
-__global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
+// W words per row, TL lanes per light row, GD gathers in flight per lane, MINB CTAs per SM
+template <int W, int TL, int GD, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2;           // lanes per row in the heavy path
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
     constexpr int64_t B = 64 * W;      // sources per batch
     // light rows: TL lanes per row, VEC 16-byte chunks per lane, GD gathers in flight per lane
     constexpr int VEC = W / (2 * TL);
     constexpr int LTPW = 32 / TL;
-    constexpr int GD = (VEC == 1) ? 4 : 2;
     cg::grid_group grid = cg::this_grid();
     __shared__ Smem sm;
     __shared__ ulonglong2 s_red[TPB][T];
@@ -562,17 +561,26 @@ __global__ void __launch_bounds__(BLOCK, 2) msbfs_kernel(BfsArgs a) {
 
 }  // namespace
 
-int launch_msbfs(int W, int TL, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s) {
+int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s) {
     const void *kern = nullptr;
     if (TL == 0) TL = (W == 64) ? 16 : W / 2;
-    switch (W * 100 + TL) {
-        case 804: kern = (const void *)msbfs_kernel<8, 4>; break;
-        case 1608: kern = (const void *)msbfs_kernel<16, 8>; break;
-        case 1604: kern = (const void *)msbfs_kernel<16, 4>; break;
-        case 3216: kern = (const void *)msbfs_kernel<32, 16>; break;
-        case 3208: kern = (const void *)msbfs_kernel<32, 8>; break;
-        case 6432: kern = (const void *)msbfs_kernel<64, 32>; break;
-        case 6416: kern = (const void *)msbfs_kernel<64, 16>; break;
+    const int vec = W / (2 * TL);
+    const int minb = blocks_per_sm == 1 ? 1 : 2;
+    if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : 2);
+    switch ((W * 100 + TL) * 100 + GD * 10 + minb) {
+        case 80442: kern = (const void *)msbfs_kernel<8, 4, 4, 2>; break;
+        case 80481: kern = (const void *)msbfs_kernel<8, 4, 8, 1>; break;
+        case 160881: kern = (const void *)msbfs_kernel<16, 8, 8, 1>; break;
+        case 160842: kern = (const void *)msbfs_kernel<16, 8, 4, 2>; break;
+        case 160422: kern = (const void *)msbfs_kernel<16, 4, 2, 2>; break;
+        case 321642: kern = (const void *)msbfs_kernel<32, 16, 4, 2>; break;
+        case 321681: kern = (const void *)msbfs_kernel<32, 16, 8, 1>; break;
+        case 320822: kern = (const void *)msbfs_kernel<32, 8, 2, 2>; break;
+        case 643242: kern = (const void *)msbfs_kernel<64, 32, 4, 2>; break;
+        case 641622: kern = (const void *)msbfs_kernel<64, 16, 2, 2>; break;
+        case 641641: kern = (const void *)msbfs_kernel<64, 16, 4, 1>; break;
+        case 641681: kern = (const void *)msbfs_kernel<64, 16, 8, 1>; break;
+        case 643281: kern = (const void *)msbfs_kernel<64, 32, 8, 1>; break;
         default: return -1;
     }
     const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 * 2 : 0;
@@ -580,7 +588,7 @@ int launch_msbfs(int W, int TL, const BfsArgs &a, int num_sms, int blocks_per_sm
     int maxb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, BLOCK, dyn) != cudaSuccess) return -2;
     if (maxb < 1) return -3;
-    const int b = (blocks_per_sm > 0 && blocks_per_sm < maxb) ? blocks_per_sm : maxb;
+    const int b = (minb < maxb) ? minb : maxb;
     const int grid = num_sms * b;
     BfsArgs args = a;
     void *kargs[] = {(void *)&args};

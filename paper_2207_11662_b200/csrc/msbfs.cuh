@@ -38,7 +38,8 @@ struct BfsArgs {
 // Launches the persistent cooperative kernel for W words (64*W sources per
 // batch).  Returns the grid size (< 0: no instantiation / launch failure).
 // TL = lanes per state row in the light path (0 = default: W/2, 16 at W = 64);
-// blocks_per_sm == 0 -> occupancy maximum.
-int launch_msbfs(int W, int TL, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s);
+// GD = gathers in flight per lane (0 = default for the occupancy);
+// blocks_per_sm == 1 selects the 1-CTA/SM (128-register) instantiations, else 2 CTAs/SM.
+int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s);
 
 }  // namespace hm

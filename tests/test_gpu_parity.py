@@ -77,7 +77,7 @@ def test_psi_special(hm, name, V, E):
     E = {(min(u, v), max(u, v)) for u, v in E if u != v}
     res = O.analyze(V, E)
     # narrow batches (B = 512: several batches per component), other team widths and occupancies
-    for words, team, bps, unit in ((8, 0, 0, 8), (16, 4, 1, 16), (64, 32, 0, 32), (64, 16, 0, 8)):
+    for words, team, bps, unit in ((8, 0, 0, 8), (16, 4, 0, 16), (64, 32, 1, 32), (64, 16, 1, 8), (32, 16, 1, 32)):
         with hm() as ctx:
             ctx.set_param("bfs_words", words)
             ctx.set_param("bfs_unit", unit)

@@ -29,7 +29,7 @@ for r in rows[2:]:
 res = {"config": cfg, "bfs_words": words, "bfs_hints": hints, "launches": len(per),
        "dram_bytes_per_launch": sum(p["dram_bytes"] for p in per) / max(1, len(per)),
        "per_launch": per,
-       "source": "ncu --set full --clock-control none, the MS-BFS launches of bench.py's setup pass "
+       "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none (tools/gpu_traffic.sh), the MS-BFS launches of bench.py's setup pass "
                  "(3 layers + AND graph of one HoMLN); ncu replays are serialised and cold-cache"}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in res.items() if k != "per_launch"}))
