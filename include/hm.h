@@ -64,6 +64,7 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (1, or 0 / 2 = two)
  *   "bfs_gd"      : MS-BFS neighbour-row gathers in flight per lane (0 = default, 2, 4, 8)
+ *   "bfs_interleave": 1 (default) CTAs own interleaved light-path units, 0 contiguous ranges
  *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
  *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16 or 8)

@@ -354,6 +354,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
     a.hints = ctx->params.bfs_hints;
+    a.interleave = ctx->params.bfs_interleave;
+    a.dbg_level = ctx->params.bfs_dbg >> 8;                   // bfs_dbg bits 8.. (profiling builds)
     a.unit_shift = ctx->params.bfs_unit == 8 ? 2 : ctx->params.bfs_unit == 16 ? 1 : 0;
     a.chg_smem = (ctx->params.bfs_chg_smem && bmw * 4 * 2 <= 80 * 1024) ? 1 : 0;
     a.S = Srel.as<uint64_t>();

@@ -87,6 +87,7 @@ struct Params {
     int bfs_heavy = 256;
     int bfs_blocks_per_sm = 0;
     int bfs_chg_smem = 1;
+    int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
     int bfs_unit = 32;         // MS-BFS light-path rows per work unit (32, 16, 8)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)

@@ -31,7 +31,9 @@ struct BfsArgs {
     int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
     int unit_shift;
-    int hints;                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
+    int interleave;              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
+    int hints;
+    int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
                                  // 4 F_d stores evict_last, 8 F_d stores evict_first              // light-path work unit = 32 >> unit_shift rows of a 32-row group
 };
 

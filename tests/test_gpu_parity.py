@@ -118,8 +118,9 @@ def test_tuning_invariance(hm):
     for words in (8, 16, 32, 64):
         for heavy in (4, 64, 100000):
             for bps in (0, 1):
-                for chg_smem, unit in ((0, 32), (1, 8)):
+                for chg_smem, unit, inter in ((0, 32, 0), (1, 8, 1)):
                     with hm() as ctx:
+                        ctx.set_param("bfs_interleave", inter)
                         ctx.set_param("bfs_unit", unit)
                         ctx.set_param("bfs_words", words)
                         ctx.set_param("bfs_heavy", heavy)

@@ -10,6 +10,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--graph", default="0")
 ap.add_argument("--set", action="append", default=[], help="name=value library parameter")
+ap.add_argument("--level", type=int, default=0, help="profile only this BFS level (HM_MSBFS_PROF builds)")
 a = ap.parse_args()
 h = build_config(a.config)
 with Context(0) as ctx:
@@ -21,7 +22,7 @@ with Context(0) as ctx:
     g = ctx.and_aggregate(list(h.subsets[0])) if a.graph == "and" else int(a.graph)
     ctx.closeness(g, out={})
     ctx.sync(); ctx.stats(reset=True)
-    ctx.set_param("bfs_dbg", 2)
+    ctx.set_param("bfs_dbg", 2 | (a.level << 8))
     ctx.closeness(g, out={})
     ctx.sync()
     st = ctx.stats()
@@ -43,4 +44,5 @@ if ph.sum() > 0:
     nwarps = 148 * 32
     rounds, iters = float(dc[8200]), float(dc[8201])
     print(f"  per warp: rounds {rounds / nwarps:.0f}, gather iterations {iters / nwarps:.0f}; "
-          f"cycles per round {ph[5] / max(rounds, 1):.0f}, per level-step per warp {ph.sum() / nwarps / max(cnt.sum(), 1):.0f}")
+          f"cycles per round {ph[5] / max(rounds, 1):.0f}, "
+          f"per level-step per warp {ph.sum() / nwarps / max(cnt[a.level] if a.level else cnt.sum(), 1):.0f}")
