@@ -1,5 +1,6 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration
-bench.py times (default parameters: 2048 sources per batch).
+bench.py times (the library defaults: 4096 sources per batch, 16-lane row teams,
+L2 policy hints, interleaved work units).
 
 The oracle cannot run all-sources BFS at these sizes in test time, so:
   * S, k, closeness, pen: exact on seeded samples of vertices, each checked
