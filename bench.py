@@ -156,18 +156,32 @@ def run_ours(args, rank, world, local_rank):
     W_total = sum(units)
     arcs = [2 * ctx.graph_info(i)[1] for i in range(len(h.layers))] + arcs_and
 
-    def hot_step():
-        if (not args.fused):
-            for i in range(len(h.layers)):
-                ctx.closeness(i, out={})
-        ands = []
-        for T in h.subsets:
-            g = ctx.and_aggregate(list(T))
-            if (not args.fused):
+    # --shard (SURVEY §8(f) rank 4, strong scaling of ONE HoMLN): rank r runs the source
+    # batches r, r + N, ... of every graph, one NCCL all-reduce sums the partial distance
+    # sums of all graphs of the step, then every rank finalises and composes.
+    n_graphs = len(h.layers) + len(h.subsets)
+    S_all = torch.zeros(n_graphs * V, dtype=torch.int64, device=f"cuda:{dev}") if args.shard else None
+
+    def psi(gids):
+        """closeness of the graphs gids (plain, fused or sharded)"""
+        if args.shard:
+            for k, g in enumerate(gids):
+                ctx.closeness_partial(g, rank, world, out=S_all[k * V:(k + 1) * V])
+            if world > 1:
+                import torch.distributed as dist
+                with torch.cuda.stream(s):
+                    dist.all_reduce(S_all[:len(gids) * V], op=dist.ReduceOp.SUM)
+            for k, g in enumerate(gids):
+                ctx.closeness_combine(g, S_all[k * V:(k + 1) * V])
+        elif args.fused:
+            ctx.closeness_multi(list(gids))
+        else:
+            for g in gids:
                 ctx.closeness(g, out={})
-            ands.append(g)
-        if not (not args.fused):            # layers + ground-truth graphs in one fused MS-BFS pass (--fused)
-            ctx.closeness_multi(list(range(len(h.layers))) + ands)
+
+    def hot_step():
+        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        psi(list(range(len(h.layers))) + ands)
         for T, g in zip(h.subsets, ands):
             ctx.topk_closeness(g, K, out=ids_dev)
             ctx.compose("cc2", list(T), K, out=ids_dev)
@@ -206,7 +220,8 @@ def run_ours(args, rank, world, local_rank):
     ms = [a.elapsed_time(b) for a, b in times]
     st = ctx.stats(reset=True)
     total_ms = float(sum(ms))
-    value, total_ms = job_value(W_total * args.steps, total_ms, device=f"cuda:{dev}")
+    share = W_total / world if args.shard else W_total       # units this rank processed per step
+    value, total_ms = job_value(share * args.steps, total_ms, device=f"cuda:{dev}")
     ms_per_step = total_ms / args.steps
 
     # ---- e2e: host edge lists -> public API -> host results, copies inside the timed region
@@ -225,11 +240,7 @@ def run_ours(args, rank, world, local_rank):
             ctx.load_layers(V, host_layers)                 # H2D from pinned host memory
             outs = []
             ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
-            if (not args.fused):
-                for g in list(range(len(h.layers))) + ands:
-                    ctx.closeness(g, out={})
-            else:
-                ctx.closeness_multi(list(range(len(h.layers))) + ands)
+            psi(list(range(len(h.layers))) + ands)
             for T, g in zip(h.subsets, ands):
                 outs.append(ctx.topk_closeness(g, K))       # D2H of every result list
                 outs.append(ctx.compose("cc2", list(T), K)[0])
@@ -241,7 +252,7 @@ def run_ours(args, rank, world, local_rank):
             e_ms.append(e0.elapsed_time(e1))
             d2h = sum(int(o.nbytes) for o in outs)
         e2e_ms = float(np.mean(e_ms))
-        e2e_val, e2e_ms = job_value(W_total, e2e_ms, device=f"cuda:{dev}")
+        e2e_val, e2e_ms = job_value(share, e2e_ms, device=f"cuda:{dev}")
         e2e = {"value": e2e_val, "unit": "TEPS", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
@@ -279,12 +290,14 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",
         "value": value, "unit": "TEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if args.shard else "weak",
+        "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": h.name, "V": V, "layers": len(h.layers), "subsets": [list(t) for t in h.subsets],
                    "K": K, "recipe": h.recipe, "units_W": W_total, "units_per_graph": dict(zip(graph_names, units)),
                    "bfs_words": args.words, "bfs_hints": args.hints, "sources_per_batch": 64 * args.words,
-                   "l2": "flushed (256 MiB write) before each timed step", "parallelism": f"replicas{world}"},
+                   "l2": "flushed (256 MiB write) before each timed step",
+                   "parallelism": f"batch-shard{world}+nccl-allreduce(S)" if args.shard else f"replicas{world}"},
         "s_per_homln": ms_per_step / 1e3,
         "e2e": e2e, "roofline": roof, "clocks": clocks, "gpu_launches": int(round(launches_per_step)),
     }
@@ -416,6 +429,8 @@ def main():
     ap.add_argument("--hints", type=int, default=11, help="MS-BFS L2 eviction-priority bits (library bfs_hints)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: split every graph's source batches over the ranks, NCCL all-reduce of S")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     args = ap.parse_args()

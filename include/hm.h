@@ -135,6 +135,21 @@ hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reac
  * -> ESTATE; sum of V >= 2^26 -> ERANGE. */
 hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n);
 
+/* Sharded Psi (source batches split over GPUs, one sum
+ * reduction).  hm_closeness_partial runs the all-sources BFS of graph g for the
+ * source batches i = shard, shard + nshards, ... only (the batch order is fixed by
+ * the graph) and writes that shard's partial target-side distance sums,
+ * uint64[V] in original vertex order (0 for isolated vertices), to S_partial
+ * (host or device).  The element-wise sum over all nshards shards is exactly
+ * S (each batch contributes once), e.g. after an NCCL all-reduce.
+ * hm_closeness_combine finalises graph g from that sum S_total (host or device,
+ * uint64[V]): k, closeness, n-penalty sum, degrees, mean and CC nodes, cached
+ * exactly as hm_closeness caches them (hm_closeness_results / hm_compose /
+ * hm_topk_closeness then work unchanged).  Errors: nshards < 1 or shard outside
+ * [0, nshards) or NULL buffer -> EINVAL; unknown graph -> ESTATE. */
+hm_status hm_closeness_partial(hm_ctx *ctx, int32_t g, int32_t shard, int32_t nshards, uint64_t *S_partial);
+hm_status hm_closeness_combine(hm_ctx *ctx, int32_t g, const uint64_t *S_total);
+
 /* Copy the cached hm_closeness results of graph g (ESTATE if none); the same
  * four outputs as hm_closeness, each NULL-able, host or device, length V. */
 hm_status hm_closeness_results(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,

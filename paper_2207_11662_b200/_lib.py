@@ -39,6 +39,8 @@ SIGNATURES = {
     "hm_closeness": (ctypes.c_int32, [vp, ctypes.c_int32, vp, vp, vp, vp]),
     "hm_closeness_multi": (ctypes.c_int32, [vp, c_i32p, ctypes.c_int32]),
     "hm_closeness_results": (ctypes.c_int32, [vp, ctypes.c_int32, vp, vp, vp, vp]),
+    "hm_closeness_partial": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp]),
+    "hm_closeness_combine": (ctypes.c_int32, [vp, ctypes.c_int32, vp]),
     "hm_cc_nodes": (ctypes.c_int32, [vp, ctypes.c_int32, vp, c_i32p, ctypes.POINTER(ctypes.c_double)]),
     "hm_degrees": (ctypes.c_int32, [vp, ctypes.c_int32, vp]),
     "hm_topk_closeness": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int32, vp]),

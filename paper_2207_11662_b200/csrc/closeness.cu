@@ -153,13 +153,20 @@ __global__ void k_union_copy(const int32_t *__restrict__ rp, const int32_t *__re
 }
 
 // per-graph finalize; union arrays are indexed at voff + v
+// S from the relabelled accumulators (S_orig == nullptr) or given in original order
+// (hm_closeness_combine: the sum of the shards' partial sums).
 __global__ void k_finalize(const int32_t *old_to_new, const int32_t *label, const int32_t *csize,
                            const int32_t *row_ptr, const uint64_t *S_rel, const int32_t *scalars,
+                           const uint64_t *S_orig,
                            uint64_t *S, int32_t *kk, double *c, uint64_t *pen, int32_t *deg, int V, int voff) {
-    const int n_live = scalars[0];
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
-        const int i = old_to_new[voff + v];
-        const uint64_t s = (i < n_live) ? S_rel[i] : 0ull;
+        uint64_t s;
+        if (S_orig) {
+            s = S_orig[v];
+        } else {
+            const int i = old_to_new[voff + v];
+            s = (i < scalars[0]) ? S_rel[i] : 0ull;
+        }
         const int k = csize[label[voff + v]];
         // Wasserman-Faust closeness exactly as NetworkX evaluates it:
         // ((k-1)/S) * ((k-1)/(V-1)), binary64 RN, 0 if S == 0 or V <= 1.
@@ -174,6 +181,16 @@ __global__ void k_finalize(const int32_t *old_to_new, const int32_t *label, cons
         c[v] = cv;
         pen[v] = s + (uint64_t)(V - k) * (uint64_t)V;   // n-penalty sum
         deg[v] = row_ptr[v + 1] - row_ptr[v];
+    }
+}
+
+// a shard's partial target-side sums in original vertex order (0 for isolated vertices)
+__global__ void k_partial_sums(const int32_t *old_to_new, const uint64_t *S_rel, const int32_t *scalars,
+                               uint64_t *S_out, int V) {
+    const int n_live = scalars[0];
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const int i = old_to_new[v];
+        S_out[v] = (i < n_live) ? S_rel[i] : 0ull;
     }
 }
 
@@ -201,14 +218,53 @@ inline int nbits(uint64_t x) {
 
 }  // namespace
 
+// 5.-6. finalize one graph: S, k, WF closeness, n-penalty sum, degree; exact mean; CH bitmap
+static void finalize_graph(hm_ctx *ctx, Graph &G, const int32_t *o2n, const int32_t *label, const int32_t *csize,
+                           const uint64_t *S_rel, const int32_t *scalars, const uint64_t *S_orig, int voff) {
+    cudaStream_t s = ctx->stream;
+    const int Vg = G.V;
+    k_finalize<<<grid_for(Vg, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(
+        o2n, label, csize, G.row_ptr.as<int32_t>(), S_rel, scalars, S_orig, G.S.as<uint64_t>(), G.k.as<int32_t>(),
+        G.c.as<double>(), G.pen.as<uint64_t>(), G.deg.as<int32_t>(), Vg, voff);
+    check_launch("k_finalize");
+    count_launch(ctx);
+    uint32_t *chbm = G.ch.as<uint32_t>();
+    const size_t nbw = (size_t)(Vg + 31) / 32;
+    double *d_mu = reinterpret_cast<double *>(reinterpret_cast<char *>(chbm) + ((nbw * 4 + 7) / 8) * 8);
+    int32_t *d_cnt = reinterpret_cast<int32_t *>(d_mu + 1);
+    exact_mean(ctx, G.c.as<double>(), Vg, nullptr, d_mu, nullptr);
+    HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
+    k_cc_bitmap<<<grid_for((int64_t)Vg, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(G.c.as<double>(), d_mu, chbm,
+                                                                                    d_cnt, Vg);
+    check_launch("k_cc_bitmap");
+    count_launch(ctx);
+    G.has_results = true;
+}
+
 void closeness(hm_ctx *ctx, Graph &G) { closeness_multi(ctx, std::vector<Graph *>{&G}); }
+
+void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out) {
+    closeness_multi(ctx, std::vector<Graph *>{&G}, shard, nshards, d_S_out, nullptr);
+}
+
+void closeness_combine(hm_ctx *ctx, Graph &G, const uint64_t *d_S_total) {
+    closeness_multi(ctx, std::vector<Graph *>{&G}, 0, 1, nullptr, d_S_total);
+}
 
 // Psi for several graphs in one fused pass over their disjoint union (each
 // graph is its own set of components; the MS-BFS batches all of them
 // together, so the per-level costs are shared).  Results are per graph.
-void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
+//
+// Sharding: with d_S_partial the MS-BFS runs only the batches
+// i = shard, shard + nshards, ... and the raw partial sums are written out instead of
+// being finalised; with d_S_total the MS-BFS is skipped and the graph is finalised from
+// the given (summed) sums.  Both are single-graph modes.
+void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int nshards, uint64_t *d_S_partial,
+                     const uint64_t *d_S_total) {
     cudaStream_t s = ctx->stream;
     HM_REQUIRE(!gs.empty(), HM_EINVAL, "no graphs");
+    HM_REQUIRE(nshards >= 1 && shard >= 0 && shard < nshards, HM_EINVAL, "need 0 <= shard < nshards");
+    HM_REQUIRE(!(d_S_partial || d_S_total) || gs.size() == 1, HM_EINVAL, "sharded closeness is per graph");
     int64_t Vu64 = 0, nnz_u = 0;
     for (Graph *g : gs) {
         Vu64 += g->V;
@@ -282,6 +338,12 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     check_launch("cc");
     count_launch(ctx, 3);
 
+    if (d_S_total) {
+        Graph &G = *gs[0];
+        finalize_graph(ctx, G, nullptr, label.as<int32_t>(), csize.as<int32_t>(), nullptr, scalars, d_S_total, 0);
+        return;
+    }
+
     // 2. component order and vertex order
     k_comp_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), csize.as<int32_t>(), key1.as<uint64_t>(), V);
     count_launch(ctx);
@@ -354,6 +416,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
     a.hints = ctx->params.bfs_hints;
+    a.shard = shard;
+    a.nshards = nshards;
     a.interleave = ctx->params.bfs_interleave;
     a.dbg_level = ctx->params.bfs_dbg >> 8;                   // bfs_dbg bits 8.. (profiling builds)
     a.unit_shift = ctx->params.bfs_unit == 8 ? 2 : ctx->params.bfs_unit == 16 ? 1 : 0;
@@ -388,30 +452,16 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     count_launch(ctx);
     ctx->stats.bfs_launches += 1;
 
-    for (size_t gi = 0; gi < gs.size(); ++gi) {
-        Graph &G = *gs[gi];
-        const int Vg = G.V;
-        // 5. finalize (the graph's own V for closeness and the n-penalty)
-        k_finalize<<<grid_for(Vg, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(
-            o2n.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(), G.row_ptr.as<int32_t>(),
-            Srel.as<uint64_t>(), scalars, G.S.as<uint64_t>(), G.k.as<int32_t>(), G.c.as<double>(),
-            G.pen.as<uint64_t>(), G.deg.as<int32_t>(), Vg, voff[gi]);
-        check_launch("k_finalize");
+    if (d_S_partial) {
+        k_partial_sums<<<grid_for(V, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(o2n.as<int32_t>(), Srel.as<uint64_t>(),
+                                                                                 scalars, d_S_partial, V);
+        check_launch("k_partial_sums");
         count_launch(ctx);
-
-        // 6. mean closeness (exact) and CC nodes
-        uint32_t *chbm = G.ch.as<uint32_t>();
-        const size_t nbw = (size_t)(Vg + 31) / 32;
-        double *d_mu = reinterpret_cast<double *>(reinterpret_cast<char *>(chbm) + ((nbw * 4 + 7) / 8) * 8);
-        int32_t *d_cnt = reinterpret_cast<int32_t *>(d_mu + 1);
-        exact_mean(ctx, G.c.as<double>(), Vg, nullptr, d_mu, nullptr);
-        HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
-        k_cc_bitmap<<<grid_for((int64_t)Vg, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(G.c.as<double>(), d_mu,
-                                                                                        chbm, d_cnt, Vg);
-        check_launch("k_cc_bitmap");
-        count_launch(ctx);
-        G.has_results = true;
+        return;
     }
+    for (size_t gi = 0; gi < gs.size(); ++gi)
+        finalize_graph(ctx, *gs[gi], o2n.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(), Srel.as<uint64_t>(),
+                       scalars, nullptr, voff[gi]);
 }
 
 }  // namespace hm

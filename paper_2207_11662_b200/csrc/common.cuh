@@ -145,7 +145,10 @@ void build_csr(hm_ctx *ctx, int32_t V, const int32_t *edges_host_or_dev, int64_t
                int64_t *dropped);
 void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, Graph &out);
 void closeness(hm_ctx *ctx, Graph &G);
-void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs);
+void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard = 0, int nshards = 1,
+                     uint64_t *d_S_partial = nullptr, const uint64_t *d_S_total = nullptr);
+void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out);
+void closeness_combine(hm_ctx *ctx, Graph &G, const uint64_t *d_S_total);
 // exact (correctly rounded) sum of masked non-negative doubles, then mean = sum / count;
 // result written to device double *d_mean (count taken from mask popcount or n)
 void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask_or_null,

@@ -266,6 +266,38 @@ hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n) {
     HM_API_END(ctx)
 }
 
+hm_status hm_closeness_partial(hm_ctx *ctx, int32_t g, int32_t shard, int32_t nshards, uint64_t *S_partial) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(S_partial, HM_EINVAL, "null S_partial");
+    HM_REQUIRE(nshards >= 1 && shard >= 0 && shard < nshards, HM_EINVAL, "need 0 <= shard < nshards");
+    Graph &G = graph(ctx, g);
+    const size_t V = (size_t)G.V;
+    if (is_device_ptr(S_partial)) {
+        closeness_partial(ctx, G, shard, nshards, S_partial);
+    } else {
+        Buf tmp(V * 8, ctx->stream);
+        closeness_partial(ctx, G, shard, nshards, tmp.as<uint64_t>());
+        copy_out(ctx, S_partial, tmp.p, V * 8);
+    }
+    HM_API_END(ctx)
+}
+
+hm_status hm_closeness_combine(hm_ctx *ctx, int32_t g, const uint64_t *S_total) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(S_total, HM_EINVAL, "null S_total");
+    Graph &G = graph(ctx, g);
+    const size_t V = (size_t)G.V;
+    if (is_device_ptr(S_total)) {
+        closeness_combine(ctx, G, S_total);
+    } else {
+        Buf tmp(V * 8, ctx->stream);
+        HM_CUDA(cudaMemcpyAsync(tmp.p, S_total, V * 8, cudaMemcpyHostToDevice, ctx->stream));
+        closeness_combine(ctx, G, tmp.as<uint64_t>());
+        HM_CUDA(cudaStreamSynchronize(ctx->stream));   // the host buffer may be reused on return
+    }
+    HM_API_END(ctx)
+}
+
 hm_status hm_closeness_results(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach, double *closeness_out,
                                uint64_t *pen_sum) {
     HM_API_BEGIN(ctx)

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     Prof pf;
     PROF_INIT(pf);
 
-    for (int64_t base = 0; base < n_giant; base += B) {
+    for (int64_t base = (int64_t)a.shard * B; base < n_giant; base += (int64_t)a.nshards * B) {
         if (threadIdx.x == 0) sm.hi = batch_hi(a, base, n_comp, n_live);
         __syncthreads();
         const int hi = sm.hi;

@@ -31,6 +31,7 @@ struct BfsArgs {
     int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
     int unit_shift;
+    int shard, nshards;          // run batches i = shard, shard + nshards, ... only
     int interleave;              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
     int hints;
     int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,

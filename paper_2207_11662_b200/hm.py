@@ -178,6 +178,20 @@ class Context:
         arr = (ctypes.c_int32 * len(gids))(*gids)
         self._check(self.L.hm_closeness_multi(self.h, arr, len(gids)))
 
+    def closeness_partial(self, g, shard, nshards, out=None):
+        """One shard's partial distance sums S_partial[V] (uint64; numpy, or into a
+        device tensor `out`): batches shard, shard + nshards, ... (hm_closeness_partial)."""
+        V, _ = self.graph_info(g)
+        buf = np.zeros(V, np.uint64) if out is None else out
+        self._check(self.L.hm_closeness_partial(self.h, int(g), int(shard), int(nshards), _ptr(buf)))
+        return buf
+
+    def closeness_combine(self, g, S_total):
+        """Finalise graph g from the summed shard sums (numpy uint64 or device tensor)."""
+        if isinstance(S_total, np.ndarray):
+            S_total = np.ascontiguousarray(S_total, dtype=np.uint64)
+        self._check(self.L.hm_closeness_combine(self.h, int(g), _ptr(S_total)))
+
     def closeness_results(self, g, out=None, want=("S", "k", "c", "pen")):
         """Cached closeness results of graph g (numpy by default, or into ``out``)."""
         V, _ = self.graph_info(g)

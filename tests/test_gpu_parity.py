@@ -316,3 +316,39 @@ def test_closeness_multi_fused(hm, name, V):
             check_psi(h.V, Es[i], fused[i])
         for T, g in zip(h.subsets, ands):
             check_psi(h.V, O.and_aggregate([Es[i] for i in T]), fused[g])
+
+
+# ---------------------------------------------------------------------------
+# Sharded Psi: partial sums over source-batch shards add up
+# to S exactly, and finalising from the sum reproduces every cached result
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,V", [("C5", 8192), ("C3", 2048), ("C4", 2048)])
+def test_sharded_closeness(hm, name, V):
+    h = build_config(name, V=V)
+    with hm() as ctx:
+        ctx.set_param("bfs_words", 8)                   # B = 512: several batches per graph
+        ctx.load_layers(h.V, h.layers)
+        T = list(h.subsets[0])
+        gids = list(range(len(h.layers))) + [ctx.and_aggregate(T)]
+        full = {}
+        for g in gids:
+            full[g] = ctx.closeness(g)
+            full[g]["topk"] = ctx.topk_closeness(g, h.K).tolist()
+        ref_cc2 = ctx.compose("cc2", T, h.K)[0].tolist()
+        ref_cc1 = ctx.compose("cc1", T, h.K)
+        for nshards in (1, 2, 3):
+            for g in gids:
+                parts = [ctx.closeness_partial(g, r, nshards) for r in range(nshards)]
+                tot = np.sum(np.stack(parts).astype(np.uint64), axis=0, dtype=np.uint64)
+                assert tot.tolist() == full[g]["S"].tolist(), (g, nshards)
+                ctx.closeness_combine(g, tot)
+                got = ctx.closeness_results(g)
+                for key in ("S", "k", "pen"):
+                    assert got[key].tolist() == full[g][key].tolist()
+                assert np.array_equal(got["c"].view(np.uint64), full[g]["c"].view(np.uint64))
+                assert ctx.topk_closeness(g, h.K).tolist() == full[g]["topk"]
+            assert ctx.compose("cc2", T, h.K)[0].tolist() == ref_cc2
+            ids, n = ctx.compose("cc1", T, h.K)
+            assert n == ref_cc1[1] and ids.tolist() == ref_cc1[0].tolist()
+        with pytest.raises(Exception):
+            ctx.closeness_partial(gids[0], 2, 2)
