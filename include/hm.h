@@ -64,6 +64,8 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (1, or 0 / 2 = two)
  *   "bfs_gd"      : MS-BFS neighbour-row gathers in flight per lane (0 = default, 2, 4, 8)
+ *   "bfs_prune"   : 1 (default) exact 2-core pruning of the largest component before the MS-BFS
+ *                   (hanging trees restored by weights and re-rooting; results unchanged), 0 off
  *   "bfs_interleave": 1 (default) CTAs own interleaved light-path units, 0 contiguous ranges
  *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
@@ -138,10 +140,13 @@ hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n);
 /* Sharded Psi (source batches split over GPUs, one sum
  * reduction).  hm_closeness_partial runs the all-sources BFS of graph g for the
  * source batches i = shard, shard + nshards, ... only (the batch order is fixed by
- * the graph) and writes that shard's partial target-side distance sums,
- * uint64[V] in original vertex order (0 for isolated vertices), to S_partial
- * (host or device).  The element-wise sum over all nshards shards is exactly
- * S (each batch contributes once), e.g. after an NCCL all-reduce.
+ * the graph) and writes that shard's partial target-side sums, uint64[V] in
+ * original vertex order, to S_partial (host or device).  The element-wise sum
+ * over all nshards shards (e.g. an NCCL all-reduce) is the graph's
+ * pre-finalisation sum vector, the same for every nshards (each batch
+ * contributes once): S itself when "bfs_prune" is 0, else the pruned core's
+ * weighted sums (peeled vertices 0).  Only that sum is meaningful, through
+ * hm_closeness_combine.
  * hm_closeness_combine finalises graph g from that sum S_total (host or device,
  * uint64[V]): k, closeness, n-penalty sum, degrees, mean and CC nodes, cached
  * exactly as hm_closeness caches them (hm_closeness_results / hm_compose /

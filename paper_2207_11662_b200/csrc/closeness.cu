@@ -104,12 +104,14 @@ __global__ void k_nlive(const int32_t *size_s, const int32_t *cstart, int32_t *s
         if (size_s[i] > 1 && (i + 1 == n_comp || size_s[i + 1] <= 1)) scalars[0] = cstart[i] + size_s[i];
 }
 
-__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, uint64_t *key, int V) {
+// peeled vertices (rem != nullptr, rem[v] > 0) sort after every component: no BFS row
+__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, const int32_t *rem, uint64_t *key,
+                            int V) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-        key[v] = ((uint64_t)rank_of_root[label[v]] << 32) | (uint32_t)v;
+        key[v] = ((rem && rem[v]) ? ((uint64_t)V << 32) : ((uint64_t)rank_of_root[label[v]] << 32)) | (uint32_t)v;
 }
 
-__global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32_t *size_s,
+__global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32_t *degl, const int32_t *size_s,
                        const int32_t *cstart, int32_t *new_to_old, int32_t *old_to_new,
                        int32_t *new_deg, int2 *cinfo, int V) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
@@ -118,7 +120,13 @@ __global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32
         const int r = (int)(k >> 32);
         new_to_old[i] = old;
         old_to_new[old] = i;
-        new_deg[i] = row_ptr[old + 1] - row_ptr[old];
+        if (r >= V) {                       // peeled vertex: no row
+            new_deg[i] = 0;
+            cinfo[i] = make_int2(0, 0);
+            continue;
+        }
+        // live degree: arcs to peeled vertices are dropped (degl counts live neighbours)
+        new_deg[i] = degl ? degl[old] : row_ptr[old + 1] - row_ptr[old];
         cinfo[i] = make_int2(cstart[r], size_s[r]);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) new_deg[V] = 0;
@@ -127,7 +135,7 @@ __global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32
 __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const int32_t *__restrict__ nrp, const int32_t *__restrict__ new_to_old,
                                const int32_t *__restrict__ old_to_new, int32_t *__restrict__ ncol,
-                               int32_t *heavy, int32_t *scalars, int heavy_deg, int V) {
+                               int32_t *heavy, int32_t *scalars, int heavy_deg, const int32_t *rem, int V) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -136,11 +144,26 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
         const int old = new_to_old[i];
         const int rb = row_ptr[old], re = row_ptr[old + 1];
         const int ob = nrp[i];
-        // packed arc: (relabelled neighbour << 5) | (row index within its 32-row group)
-        for (int j = rb + lane; j < re; j += 32)
-            ncol[ob + (j - rb)] = (old_to_new[col[j]] << 5) | (int)(i & 31);
-        if (lane == 0 && re - rb > heavy_deg) heavy[atomicAdd(scalars + 3, 1)] = (int)i;
+        // packed arc: (relabelled neighbour << 5) | (row index within its 32-row group);
+        // with pruning only arcs to live (unpeeled) neighbours, order kept
+        int outn = 0;
+        for (int j0 = rb; j0 < re; j0 += 32) {
+            const int j = j0 + lane;
+            const int u = j < re ? col[j] : 0;
+            const bool keep = j < re && !(rem && rem[u]);
+            const unsigned b = __ballot_sync(0xffffffffu, keep);
+            if (keep) ncol[ob + outn + __popc(b & ((1u << lane) - 1u))] = (old_to_new[u] << 5) | (int)(i & 31);
+            outn += __popc(b);
+        }
+        if (lane == 0 && outn > heavy_deg) heavy[atomicAdd(scalars + 3, 1)] = (int)i;
     }
+}
+
+// hanging-tree size T of every BFS row (weights of the pruned MS-BFS)
+__global__ void k_row_T(const int32_t *new_to_old, const uint32_t *tsz, const int32_t *scalars, uint32_t *T) {
+    const int n_live = scalars[0];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x)
+        T[i] = tsz[new_to_old[i]] - 1u;
 }
 
 // union CSR of several graphs: graph g's vertex v becomes voff + v
@@ -338,14 +361,26 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     check_launch("cc");
     count_launch(ctx, 3);
 
+    // 1b. exact 2-core pruning of the largest component (prune.cu; single graph only)
+    Prune pr;
+    if (ctx->params.bfs_prune && gs.size() == 1)
+        prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr);
+    const int32_t *rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
+
     if (d_S_total) {
         Graph &G = *gs[0];
-        finalize_graph(ctx, G, nullptr, label.as<int32_t>(), csize.as<int32_t>(), nullptr, scalars, d_S_total, 0);
+        Buf Sfin((size_t)V * 8, s);
+        HM_CUDA(cudaMemcpyAsync(Sfin.p, d_S_total, (size_t)V * 8, cudaMemcpyDeviceToDevice, s));
+        if (pr.active) prune_finish(ctx, pr, label.as<int32_t>(), csize.as<int32_t>(), Sfin.as<uint64_t>(), V);
+        finalize_graph(ctx, G, nullptr, label.as<int32_t>(), csize.as<int32_t>(), nullptr, scalars,
+                       Sfin.as<uint64_t>(), 0);
         return;
     }
 
     // 2. component order and vertex order
-    k_comp_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), csize.as<int32_t>(), key1.as<uint64_t>(), V);
+    // (batching by live component sizes: the pruned component counts its core only)
+    k_comp_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), pr.active ? pr.lsize.as<int32_t>() : csize.as<int32_t>(),
+                                  key1.as<uint64_t>(), V);
     count_launch(ctx);
     {
         size_t tb = 0;
@@ -362,11 +397,12 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         size_t tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, size_s.as<int32_t>(), cstart.as<int32_t>(), V, s));
         k_nlive<<<gb, TB, 0, s>>>(size_s.as<int32_t>(), cstart.as<int32_t>(), scalars, V);
-        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), key1.as<uint64_t>(), V);
+        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem, key1.as<uint64_t>(), V);
         tbs = tb;
         HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tbs, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
                                                end_bit, s));
-        k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), U.rp, size_s.as<int32_t>(),
+        k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), U.rp, pr.active ? pr.degl.as<int32_t>() : nullptr,
+                                size_s.as<int32_t>(),
                                 cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
                                 ndeg.as<int32_t>(), cinfo.as<int2>(), V);
         tbs = tb;
@@ -378,7 +414,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     const int heavy_deg = ctx->params.bfs_heavy < BFS_MAX_LIGHT_DEG ? ctx->params.bfs_heavy : BFS_MAX_LIGHT_DEG;
     k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
                                      n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
-                                     heavy.as<int32_t>(), scalars, heavy_deg, V);
+                                     heavy.as<int32_t>(), scalars, heavy_deg, rem, V);
     check_launch("k_relabel_cols");
     count_launch(ctx);
 
@@ -416,6 +452,18 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
     a.hints = ctx->params.bfs_hints;
+    Buf Trow, planes;
+    a.tw = nullptr;
+    a.planes = nullptr;
+    if (pr.active) {                    // weights 1 + T(s) of the pruned MS-BFS (prune.cu (1))
+        Trow.alloc((size_t)V * 4, s);
+        planes.alloc((size_t)BFS_T_BITS * W * 8, s);
+        k_row_T<<<gb, TB, 0, s>>>(n2o.as<int32_t>(), pr.tsz.as<uint32_t>(), scalars, Trow.as<uint32_t>());
+        check_launch("k_row_T");
+        count_launch(ctx);
+        a.tw = Trow.as<uint32_t>();
+        a.planes = planes.as<unsigned long long>();
+    }
     a.shard = shard;
     a.nshards = nshards;
     a.interleave = ctx->params.bfs_interleave;
@@ -457,6 +505,19 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
                                                                                  scalars, d_S_partial, V);
         check_launch("k_partial_sums");
         count_launch(ctx);
+        return;
+    }
+    if (gs.size() == 1) {
+        // S in original order (weighted core sums with pruning), then (1) + (2), then finalize
+        Buf Sfin((size_t)V * 8, s);
+        k_partial_sums<<<grid_for(V, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(o2n.as<int32_t>(),
+                                                                                 Srel.as<uint64_t>(), scalars,
+                                                                                 Sfin.as<uint64_t>(), V);
+        check_launch("k_partial_sums");
+        count_launch(ctx);
+        if (pr.active) prune_finish(ctx, pr, label.as<int32_t>(), csize.as<int32_t>(), Sfin.as<uint64_t>(), V);
+        finalize_graph(ctx, *gs[0], nullptr, label.as<int32_t>(), csize.as<int32_t>(), nullptr, scalars,
+                       Sfin.as<uint64_t>(), 0);
         return;
     }
     for (size_t gi = 0; gi < gs.size(); ++gi)

@@ -87,6 +87,7 @@ struct Params {
     int bfs_heavy = 256;
     int bfs_blocks_per_sm = 0;
     int bfs_chg_smem = 1;
+    int bfs_prune = 1;         // exact 2-core pruning of the largest component before the MS-BFS
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
     int bfs_unit = 32;         // MS-BFS light-path rows per work unit (32, 16, 8)
@@ -148,6 +149,16 @@ void closeness(hm_ctx *ctx, Graph &G);
 void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard = 0, int nshards = 1,
                      uint64_t *d_S_partial = nullptr, const uint64_t *d_S_total = nullptr);
 void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out);
+
+// exact 2-core pruning of the largest component (prune.cu)
+struct Prune {
+    bool active = false;
+    int P = -1, R = 0, peeled = 0;
+    Buf rem, par, tsz, tD, degl, lsize, Cc, scal;   // per vertex / per component root
+};
+bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const int32_t *label, const int32_t *csize,
+                     int V, Prune &pr);
+void prune_finish(hm_ctx *ctx, Prune &pr, const int32_t *label, const int32_t *csize, uint64_t *S_orig, int V);
 void closeness_combine(hm_ctx *ctx, Graph &G, const uint64_t *d_S_total);
 // exact (correctly rounded) sum of masked non-negative doubles, then mean = sum / count;
 // result written to device double *d_mean (count taken from mask popcount or n)

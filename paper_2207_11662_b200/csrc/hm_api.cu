@@ -130,6 +130,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_blocks_per_sm") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_blocks_per_sm must be 0 (= 2), 1 or 2");
         ctx->params.bfs_blocks_per_sm = (int)value;
+    } else if (n == "bfs_prune") {
+        ctx->params.bfs_prune = value ? 1 : 0;
     } else if (n == "bfs_interleave") {
         ctx->params.bfs_interleave = value ? 1 : 0;
     } else if (n == "bfs_hints") {

@@ -184,7 +184,9 @@ __device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglon
 }
 
 // W words per row, TL lanes per light row, GD gathers in flight per lane, MINB CTAs per SM
-template <int W, int TL, int GD, int MINB>
+// WT: weighted sums for the pruned component (prune.cu): S(v) += d * sum over the new
+// sources s of (1 + T(s)), the T sum taken from per-batch bit planes of T in shared memory
+template <int W, int TL, int GD, int MINB, bool WT>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2;           // lanes per row in the heavy path
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
@@ -194,6 +196,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int LTPW = 32 / TL;
     cg::grid_group grid = cg::this_grid();
     __shared__ Smem sm;
+    __shared__ unsigned long long s_pl[WT ? BFS_T_BITS : 1][WT ? W : 1];   // T bit planes of the batch window
+    __shared__ int s_nb;
     __shared__ ulonglong2 s_red[TPB][T];
     extern __shared__ uint4 s_dyn[];
 
@@ -265,7 +269,29 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
         }
         if (gtid == 0) a.flags[1] = 0;
+        if (WT) {
+            // bit planes of T over the giant's source window: plane b, word w, bit j =
+            // bit b of T(row base + 64 w + j) (rows outside [0, n_giant) weigh 1: T = 0)
+            for (int64_t w = gwarp; w < W; w += nwarps) {
+                const int64_t r0 = base + 64 * w + lane, r1 = r0 + 32;
+                const uint32_t t0 = r0 < n_giant ? a.tw[r0] : 0u, t1 = r1 < n_giant ? a.tw[r1] : 0u;
+                for (int b = 0; b < BFS_T_BITS; ++b) {
+                    const unsigned lo = __ballot_sync(FULL, (t0 >> b) & 1u), hi1 = __ballot_sync(FULL, (t1 >> b) & 1u);
+                    if (lane == 0) a.planes[(size_t)b * W + w] = (unsigned long long)lo | ((unsigned long long)hi1 << 32);
+                }
+            }
+        }
         grid.sync();
+        if (WT) {
+            if (threadIdx.x == 0) s_nb = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < BFS_T_BITS * W; i += BLOCK) {
+                const unsigned long long x = a.planes[i];
+                s_pl[i / W][i % W] = x;
+                if (x) atomicMax(&s_nb, i / W + 1);
+            }
+            __syncthreads();
+        }
 
         int d = 1;
         unsigned long long t_prev = 0;
@@ -346,6 +372,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                     int cnt = __popcll(nw.x) + __popcll(nw.y);
 #pragma unroll
                     for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(tmask, cnt, o);
+                    unsigned long long wsum = 0ull;     // sum of T over the new sources (pruned component)
+                    if (WT) {
+                        const int nbp = v < n_giant ? s_nb : 0;
+                        for (int b = 0; b < nbp; ++b)
+                            wsum += (unsigned long long)(__popcll(nw.x & s_pl[b][2 * tl]) +
+                                                         __popcll(nw.y & s_pl[b][2 * tl + 1])) << b;
+#pragma unroll
+                        for (int o = T / 2; o > 0; o >>= 1) wsum += __shfl_xor_sync(tmask, wsum, o);
+                    }
                     if (cnt) {
                         st2(Fn + (size_t)v * W + 2 * tl, nw);
                         if (tl == 0) {
@@ -355,7 +390,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                             const int64_t j = (int64_t)v - ci.x - base;
                             const int kn = (int)a.K[v] + cnt;
                             a.K[v] = (uint16_t)kn;
-                            a.S[v] += (uint64_t)d * (uint64_t)cnt;
+                            a.S[v] += (uint64_t)d * ((uint64_t)cnt + wsum);
                             const uint32_t vbit = 1u << (v & 31);
                             atomicOr(&chn[v >> 5], vbit);
                             if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) atomicOr(&a.done[v >> 5], vbit);
@@ -510,6 +545,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         }
         #pragma unroll
                         for (int o = TL / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+                        unsigned long long wsum = 0ull;   // sum of T over the new sources (pruned component)
+                        if (WT) {
+                            const int nbp = (has && v < n_giant) ? s_nb : 0;
+                            const int nbw = __reduce_max_sync(FULL, (unsigned)nbp);   // warp-uniform trip count
+                            for (int b = 0; b < nbw; ++b) {
+                                unsigned c2 = 0;
+        #pragma unroll
+                                for (int q = 0; q < VEC; ++q) {
+                                    const int wi = 2 * (q * TL + ltl);
+                                    c2 += __popcll(acc[q].x & s_pl[b][wi]) + __popcll(acc[q].y & s_pl[b][wi + 1]);
+                                }
+                                if (b < nbp) wsum += (unsigned long long)c2 << b;
+                            }
+        #pragma unroll
+                            for (int o = TL / 2; o > 0; o >>= 1) wsum += __shfl_xor_sync(FULL, wsum, o);
+                        }
                         if (cnt) {
                             or_row<VEC>(acc, f0);
                             st_row<W, TL, VEC>(Fn, v, ltl, acc, pol_n);
@@ -520,7 +571,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                                 const int64_t j = (int64_t)v - ci.x - base;
                                 const int kn = Kv + cnt;
                                 a.K[v] = (uint16_t)kn;
-                                a.S[v] = Sv + (uint64_t)d * (uint64_t)cnt;
+                                a.S[v] = Sv + (uint64_t)d * ((uint64_t)cnt + wsum);
                                 cb_team |= 1u << ri;
                                 if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) db_team |= 1u << ri;
                             }
@@ -583,22 +634,27 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     const int vec = W / (2 * TL);
     const int minb = blocks_per_sm == 1 ? 1 : 2;
     if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : 2);
+#define HM_MSBFS_CASE(w, tl, gd, mb)                                                                     \
+    case ((w * 100 + tl) * 100 + gd * 10 + mb):                                                          \
+        kern = a.tw ? (const void *)msbfs_kernel<w, tl, gd, mb, true> : (const void *)msbfs_kernel<w, tl, gd, mb, false>; \
+        break;
     switch ((W * 100 + TL) * 100 + GD * 10 + minb) {
-        case 80442: kern = (const void *)msbfs_kernel<8, 4, 4, 2>; break;
-        case 80481: kern = (const void *)msbfs_kernel<8, 4, 8, 1>; break;
-        case 160881: kern = (const void *)msbfs_kernel<16, 8, 8, 1>; break;
-        case 160842: kern = (const void *)msbfs_kernel<16, 8, 4, 2>; break;
-        case 160422: kern = (const void *)msbfs_kernel<16, 4, 2, 2>; break;
-        case 321642: kern = (const void *)msbfs_kernel<32, 16, 4, 2>; break;
-        case 321681: kern = (const void *)msbfs_kernel<32, 16, 8, 1>; break;
-        case 320822: kern = (const void *)msbfs_kernel<32, 8, 2, 2>; break;
-        case 643242: kern = (const void *)msbfs_kernel<64, 32, 4, 2>; break;
-        case 641622: kern = (const void *)msbfs_kernel<64, 16, 2, 2>; break;
-        case 641641: kern = (const void *)msbfs_kernel<64, 16, 4, 1>; break;
-        case 641681: kern = (const void *)msbfs_kernel<64, 16, 8, 1>; break;
-        case 643281: kern = (const void *)msbfs_kernel<64, 32, 8, 1>; break;
+        HM_MSBFS_CASE(8, 4, 4, 2)
+        HM_MSBFS_CASE(8, 4, 8, 1)
+        HM_MSBFS_CASE(16, 8, 8, 1)
+        HM_MSBFS_CASE(16, 8, 4, 2)
+        HM_MSBFS_CASE(16, 4, 2, 2)
+        HM_MSBFS_CASE(32, 16, 4, 2)
+        HM_MSBFS_CASE(32, 16, 8, 1)
+        HM_MSBFS_CASE(32, 8, 2, 2)
+        HM_MSBFS_CASE(64, 32, 4, 2)
+        HM_MSBFS_CASE(64, 16, 2, 2)
+        HM_MSBFS_CASE(64, 16, 4, 1)
+        HM_MSBFS_CASE(64, 16, 8, 1)
+        HM_MSBFS_CASE(64, 32, 8, 1)
         default: return -1;
     }
+#undef HM_MSBFS_CASE
     const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 * 2 : 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) return -5;
     int maxb = 0;

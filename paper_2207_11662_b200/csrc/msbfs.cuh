@@ -7,6 +7,7 @@ namespace hm {
 
 // Rows of degree > min(heavy_deg, BFS_MAX_LIGHT_DEG) are processed by whole CTAs.
 constexpr int BFS_MAX_LIGHT_DEG = 1 << 30;
+constexpr int BFS_T_BITS = 24;        // pruned MS-BFS: hanging-tree sizes T < 2^24 (weight bit planes)
 
 // Device-resident description of one relabelled graph for the MS-BFS kernel.
 // Rows 0..n_live-1 are the non-isolated vertices, grouped by connected
@@ -32,7 +33,9 @@ struct BfsArgs {
     int chg_words;               // bitmap words (multiple of 4)
     int unit_shift;
     int shard, nshards;          // run batches i = shard, shard + nshards, ... only
-    int interleave;              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
+    int interleave;
+    const uint32_t *tw;          // pruned MS-BFS: hanging-tree size T per row (nullptr: unweighted)
+    unsigned long long *planes;  // [BFS_T_BITS][W] scratch: T bit planes of the batch window              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
     int hints;
     int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
                                  // 4 F_d stores evict_last, 8 F_d stores evict_first              // light-path work unit = 32 >> unit_shift rows of a 32-row group

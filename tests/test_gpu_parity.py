@@ -77,8 +77,10 @@ def test_psi_special(hm, name, V, E):
     E = {(min(u, v), max(u, v)) for u, v in E if u != v}
     res = O.analyze(V, E)
     # narrow batches (B = 512: several batches per component), other team widths and occupancies
-    for words, team, bps, unit in ((8, 0, 0, 8), (16, 4, 0, 16), (64, 32, 1, 32), (64, 16, 1, 8), (32, 16, 1, 32)):
+    for words, team, bps, unit, prune in ((8, 0, 0, 8, 1), (16, 4, 0, 16, 0), (64, 32, 1, 32, 1), (64, 16, 1, 8, 0),
+                                          (32, 16, 1, 32, 1)):
         with hm() as ctx:
+            ctx.set_param("bfs_prune", prune)
             ctx.set_param("bfs_words", words)
             ctx.set_param("bfs_unit", unit)
             ctx.set_param("bfs_team", team)
@@ -118,8 +120,9 @@ def test_tuning_invariance(hm):
     for words in (8, 16, 32, 64):
         for heavy in (4, 64, 100000):
             for bps in (0, 1):
-                for chg_smem, unit, inter in ((0, 32, 0), (1, 8, 1)):
+                for chg_smem, unit, inter, prune in ((0, 32, 0, 0), (1, 8, 1, 1)):
                     with hm() as ctx:
+                        ctx.set_param("bfs_prune", prune)
                         ctx.set_param("bfs_interleave", inter)
                         ctx.set_param("bfs_unit", unit)
                         ctx.set_param("bfs_words", words)
@@ -336,11 +339,14 @@ def test_sharded_closeness(hm, name, V):
             full[g]["topk"] = ctx.topk_closeness(g, h.K).tolist()
         ref_cc2 = ctx.compose("cc2", T, h.K)[0].tolist()
         ref_cc1 = ctx.compose("cc1", T, h.K)
+        whole = {g: ctx.closeness_partial(g, 0, 1) for g in gids}
         for nshards in (1, 2, 3):
             for g in gids:
                 parts = [ctx.closeness_partial(g, r, nshards) for r in range(nshards)]
                 tot = np.sum(np.stack(parts).astype(np.uint64), axis=0, dtype=np.uint64)
-                assert tot.tolist() == full[g]["S"].tolist(), (g, nshards)
+                # the shards add up to the unsharded pre-finalisation sums (with 2-core pruning these
+                # are the core's weighted sums; without it they are S itself)
+                assert tot.tolist() == whole[g].tolist(), (g, nshards)
                 ctx.closeness_combine(g, tot)
                 got = ctx.closeness_results(g)
                 for key in ("S", "k", "pen"):
@@ -352,3 +358,7 @@ def test_sharded_closeness(hm, name, V):
             assert n == ref_cc1[1] and ids.tolist() == ref_cc1[0].tolist()
         with pytest.raises(Exception):
             ctx.closeness_partial(gids[0], 2, 2)
+        ctx.set_param("bfs_prune", 0)                   # unpruned: the partial sums are S itself
+        for g in gids:
+            tot = ctx.closeness_partial(g, 0, 2) + ctx.closeness_partial(g, 1, 2)
+            assert tot.tolist() == full[g]["S"].tolist()
