@@ -52,11 +52,14 @@
 
 namespace cg = cooperative_groups;
 
+
+
 namespace hm {
 namespace {
 
-constexpr int BLOCK = 512;
-constexpr int NWARP = BLOCK / 32;
+// threads per CTA (2 CTAs per SM): 512 for plain sums; the weighted kernel (pruned graphs)
+// keeps more live state and runs best with 384 (85 registers instead of 64, no spills)
+constexpr int BLOCK_PLAIN = 512, BLOCK_WEIGHTED = 384;
 constexpr int CAP = 256;            // staged pairs per warp
 constexpr int SCAN_U = 4;           // arc chunks (of 32) loaded per scan step
 constexpr unsigned FULL = 0xffffffffu;
@@ -120,6 +123,7 @@ struct Prof {
 #define PROF_FLUSH(p, dst) do { } while (0)
 #endif
 
+template <int NWARP>
 struct Smem {
     int hi;
     int next;                       // next group to claim in this CTA's range
@@ -186,7 +190,7 @@ __device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglon
 // W words per row, TL lanes per light row, GD gathers in flight per lane, MINB CTAs per SM
 // WT: weighted sums for the pruned component (prune.cu): S(v) += d * sum over the new
 // sources s of (1 + T(s)), the T sum taken from per-batch bit planes of T in shared memory
-template <int W, int TL, int GD, int MINB, bool WT>
+template <int W, int TL, int GD, int MINB, bool WT, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2;           // lanes per row in the heavy path
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int VEC = W / (2 * TL);
     constexpr int LTPW = 32 / TL;
     cg::grid_group grid = cg::this_grid();
-    __shared__ Smem sm;
+    __shared__ Smem<BLOCK / 32> sm;
     __shared__ unsigned long long s_pl[WT ? BFS_T_BITS : 1][WT ? W : 1];   // T bit planes of the batch window
     __shared__ int s_nb;
     __shared__ ulonglong2 s_red[TPB][T];
@@ -232,7 +236,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     Prof pf;
     PROF_INIT(pf);
 
-    for (int64_t base = (int64_t)a.shard * B; base < n_giant; base += (int64_t)a.nshards * B) {
+    for (int64_t base = 0; base < n_giant; base += B) {
+        if (a.nshards > 1 && (int)((base / B) % a.nshards) != a.shard) continue;   // another shard's batch
         if (threadIdx.x == 0) sm.hi = batch_hi(a, base, n_comp, n_live);
         __syncthreads();
         const int hi = sm.hi;
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
         }
         if (gtid == 0) a.flags[1] = 0;
-        if (WT) {
+        if constexpr (WT) {
             // bit planes of T over the giant's source window: plane b, word w, bit j =
             // bit b of T(row base + 64 w + j) (rows outside [0, n_giant) weigh 1: T = 0)
             for (int64_t w = gwarp; w < W; w += nwarps) {
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
         }
         grid.sync();
-        if (WT) {
+        if constexpr (WT) {
             if (threadIdx.x == 0) s_nb = 0;
             __syncthreads();
             for (int i = threadIdx.x; i < BFS_T_BITS * W; i += BLOCK) {
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 #pragma unroll
                     for (int o = T / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(tmask, cnt, o);
                     unsigned long long wsum = 0ull;     // sum of T over the new sources (pruned component)
-                    if (WT) {
+                    if constexpr (WT) {
                         const int nbp = v < n_giant ? s_nb : 0;
                         for (int b = 0; b < nbp; ++b)
                             wsum += (unsigned long long)(__popcll(nw.x & s_pl[b][2 * tl]) +
@@ -390,7 +395,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                             const int64_t j = (int64_t)v - ci.x - base;
                             const int kn = (int)a.K[v] + cnt;
                             a.K[v] = (uint16_t)kn;
-                            a.S[v] += (uint64_t)d * ((uint64_t)cnt + wsum);
+                            if constexpr (WT)
+                                a.S[v] += (uint64_t)d * ((uint64_t)cnt + wsum);
+                            else
+                                a.S[v] += (uint64_t)d * (uint64_t)cnt;
                             const uint32_t vbit = 1u << (v & 31);
                             atomicOr(&chn[v >> 5], vbit);
                             if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) atomicOr(&a.done[v >> 5], vbit);
@@ -546,7 +554,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         #pragma unroll
                         for (int o = TL / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
                         unsigned long long wsum = 0ull;   // sum of T over the new sources (pruned component)
-                        if (WT) {
+                        if constexpr (WT) {
                             const int nbp = (has && v < n_giant) ? s_nb : 0;
                             const int nbw = __reduce_max_sync(FULL, (unsigned)nbp);   // warp-uniform trip count
                             for (int b = 0; b < nbw; ++b) {
@@ -571,7 +579,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                                 const int64_t j = (int64_t)v - ci.x - base;
                                 const int kn = Kv + cnt;
                                 a.K[v] = (uint16_t)kn;
-                                a.S[v] = Sv + (uint64_t)d * ((uint64_t)cnt + wsum);
+                                if constexpr (WT)
+                                    a.S[v] = Sv + (uint64_t)d * ((uint64_t)cnt + wsum);
+                                else
+                                    a.S[v] = Sv + (uint64_t)d * (uint64_t)cnt;
                                 cb_team |= 1u << ri;
                                 if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) db_team |= 1u << ri;
                             }
@@ -630,6 +641,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 
 int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s) {
     const void *kern = nullptr;
+    int block = BLOCK_PLAIN;
     if (TL == 0) TL = (W == 64) ? 16 : W / 2;
     const int vec = W / (2 * TL);
     const int minb = blocks_per_sm == 1 ? 1 : 2;
@@ -637,6 +649,7 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
 #define HM_MSBFS_CASE(w, tl, gd, mb)                                                                     \
     case ((w * 100 + tl) * 100 + gd * 10 + mb):                                                          \
         kern = a.tw ? (const void *)msbfs_kernel<w, tl, gd, mb, true> : (const void *)msbfs_kernel<w, tl, gd, mb, false>; \
+        block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;                                                     \
         break;
     switch ((W * 100 + TL) * 100 + GD * 10 + minb) {
         HM_MSBFS_CASE(8, 4, 4, 2)
@@ -658,13 +671,13 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 * 2 : 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) return -5;
     int maxb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, BLOCK, dyn) != cudaSuccess) return -2;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, block, dyn) != cudaSuccess) return -2;
     if (maxb < 1) return -3;
     const int b = (minb < maxb) ? minb : maxb;
     const int grid = num_sms * b;
     BfsArgs args = a;
     void *kargs[] = {(void *)&args};
-    if (cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(BLOCK), kargs, dyn, s) != cudaSuccess) return -4;
+    if (cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(block), kargs, dyn, s) != cudaSuccess) return -4;
     return grid;
 }
 
