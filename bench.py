@@ -268,23 +268,20 @@ def run_ours(args, rank, world, local_rank):
     n_bfs = max(1, st["bfs_launches"])
     bfs_ms_avg = st["bfs_ms"] / n_bfs
     levels_per_launch = st["bfs_levels"] / n_bfs
-    Rb = args.words * 8
-    # SURVEY §8(d) dense-level model per level: 4(V+1) row_ptr + 4A col + 3 R V state,
-    # with V and A those of one launch (the union of all graphs when fused)
-    if (not args.fused):
-        Vl, Al = V, float(np.mean(arcs))
-    else:
-        Vl, Al = V * len(arcs), float(np.sum(arcs))
-    model_bytes = levels_per_launch * (4 * (Vl + 1) + 4 * Al + 3 * Rb * Vl)
+    # SURVEY §8(d) dense-level model, accumulated by the kernel per batch over the rows and
+    # arcs that batch's BFS covers (the 2-core when pruning applies):
+    #   levels * (4 (rows + 1) row_ptr + 4 arcs col + 3 R rows state),  R = 8 W bytes per row
+    model_bytes = st["bfs_model_bytes"] / n_bfs
     achieved = model_bytes / (bfs_ms_avg / 1e3) / 1e9 if bfs_ms_avg > 0 else 0.0
     traffic, traffic_src = measured_traffic(args)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
             "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_src,
-            "kernel": "msbfs_kernel", "bytes_model": "SURVEY 8(d) dense-level: L*(4(V+1)+4A+3RV)",
+            "kernel": "msbfs_kernel",
+            "bytes_model": "SURVEY 8(d) dense-level, per batch: L*(4(rows+1)+4*arcs+3*R*rows), R=8W, summed by the kernel",
             "bytes_per_launch": model_bytes, "ms_per_launch": bfs_ms_avg,
             "levels_per_launch": levels_per_launch, "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9),
-            "launch_rows": Vl, "launch_arcs": Al, "fused_graphs": 1 if (not args.fused) else len(arcs)}
+            "fused_graphs": 1 if (not args.fused) else len(arcs)}
     launches_per_step = st["launches"] / args.steps
 
     line = {

@@ -223,6 +223,9 @@ typedef struct {
     double bfs_ms;
     int64_t bfs_levels;
     int64_t bfs_batches;
+    double bfs_model_bytes;   /* SURVEY §8(d) dense-level bytes of the MS-BFS launches, summed per batch:
+                                 levels * (4 (rows + 1) + 4 arcs + 3 * 8 W * rows) over the batch's
+                                 BFS rows and arcs (the pruned core when 2-core pruning applies) */
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
 

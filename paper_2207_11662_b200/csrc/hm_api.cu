@@ -415,8 +415,8 @@ hm_status hm_sync(hm_ctx *ctx) {
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(out, HM_EINVAL, "null out");
-    unsigned long long dv[2] = {0, 0};
-    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long dv[3] = {0, 0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto &pe : ctx->pending) {
         float ms = 0.f;
@@ -431,6 +431,7 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     out->bfs_ms = ctx->stats.bfs_ms;
     out->bfs_levels = (int64_t)dv[0];
     out->bfs_batches = (int64_t)dv[1];
+    out->bfs_model_bytes = (double)dv[2];
     if (reset) {
         ctx->stats = Stats();
         HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));

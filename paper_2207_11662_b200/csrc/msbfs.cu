@@ -632,6 +632,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         if (gtid == 0) {
             a.counters[0] += (unsigned long long)d;
             a.counters[1] += 1ull;
+            // dense-level model bytes of this batch: rows [0, hi) and their arcs
+            const unsigned long long arcs = (unsigned long long)a.row_ptr[hi];
+            a.counters[2] += (unsigned long long)d *
+                             (4ull * (hi + 1) + 4ull * arcs + 3ull * 8ull * W * (unsigned long long)hi);
         }
     }
     PROF_FLUSH(pf, a.dbgc);
