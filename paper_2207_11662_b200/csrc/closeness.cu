@@ -66,7 +66,10 @@ __global__ void k_cc_compress(int32_t *p, int32_t *label, int32_t *csize, int V)
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         const int r = cc_find(p, v);
         label[v] = r;
-        atomicAdd(csize + r, 1);
+        // warp-aggregated count (the giant component's root would serialise per-vertex atomics)
+        const unsigned act = __activemask();
+        const unsigned same = __match_any_sync(act, r);
+        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(csize + r, __popc(same));
     }
 }
 

@@ -113,9 +113,13 @@ __global__ void k_prune_stats(const int32_t *label, const int32_t *csize, const 
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         const int l = label[v];
         if (rem[v] == 0) {
-            atomicAdd(lsize + l, 1);
+            const unsigned act = __activemask();
+            const unsigned same = __match_any_sync(act, l);                 // warp-aggregated count
+            if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(lsize + l, __popc(same));
             if (l == P) {
-                atomicMax(stats + 2, (int)(tsz[v] - 1u));
+                const unsigned actp = __activemask();
+                const unsigned tmax = __reduce_max_sync(actp, tsz[v] - 1u);   // warp-aggregated max T
+                if ((threadIdx.x & 31) == __ffs(actp) - 1) atomicMax(stats + 2, (int)tmax);
                 if (tD[v]) atomicAdd(Cc + l, tD[v]);          // (1): the component constant
             }
         }
