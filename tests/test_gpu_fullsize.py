@@ -142,3 +142,39 @@ def test_fullsize_config(Context, name):
                 for v in Rset - common:
                     assert any(v in adjA[u] for u in common)
             ctx.free_graph(g)
+
+
+def test_large_vertex_count(Context):
+    """Vertex ids near the top of the supported range (V = 2^24 + 7, 16.8 M vertices,
+    mostly isolated): 64-bit state-row offsets (V x 512 B = 8.6 GB per frontier array),
+    the relabelling and the pruning paths.  A random forest plus cycles on 300 K scattered
+    vertices (many components, long hanging trees) and one 4097-vertex path; sampled
+    vertices checked with the oracle's plain BFS, isolated vertices by definition."""
+    V = (1 << 24) + 7
+    rng = np.random.default_rng(24)
+    verts = rng.choice(V, size=300_000, replace=False).astype(np.int64)
+    E = []
+    for i in range(1, len(verts)):                       # random forest on the scattered vertices
+        if rng.random() < 0.97:
+            E.append((verts[rng.integers(0, i)], verts[i]))
+    for _ in range(60_000):                               # cycles
+        a, b = rng.choice(len(verts), 2, replace=False)
+        E.append((verts[a], verts[b]))
+    path = np.arange(V - 4097, V, dtype=np.int64)          # ids up to V - 1
+    E += list(zip(path[:-1], path[1:]))
+    E = np.array(E, dtype=np.int64)
+    E = np.sort(E, axis=1)
+    E = np.unique(E[E[:, 0] != E[:, 1]], axis=0).astype(np.int32)
+    with Context() as ctx:
+        ctx.load_layers(V, [E])
+        got = ctx.closeness(0)
+        src = np.concatenate([rng.choice(verts, 24, replace=False), path[[0, 1, 2048, 4095, 4096]],
+                              [0, V - 4098]]).astype(np.int32)
+        S, k = _bfs.bfs_sources(V, E, np.sort(src), 0)
+        src = np.sort(src)
+        assert got["S"][src].tolist() == [int(x) for x in S]
+        assert got["k"][src].tolist() == [int(x) for x in k]
+        assert got["c"][src].tolist() == O.closeness_wf(V, [int(x) for x in S], [int(x) for x in k])
+        deg = np.bincount(E.reshape(-1), minlength=V)
+        iso = np.nonzero(deg == 0)[0][:1000]
+        assert not got["S"][iso].any() and (got["k"][iso] == 1).all() and not got["c"][iso].any()
