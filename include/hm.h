@@ -71,7 +71,7 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
  *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16 or 8)
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)
- *   "bfs_chg_smem": 1 (default) stages the per-level change bitmaps in shared memory, 0 reads them via L1
+ *   "bfs_chg_smem": 1 stages the per-level change bitmaps in shared memory, 0 (default) reads them via L1
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
  *   "bfs_dbg"     : debug bits (1 = per-thread fence before grid barriers, 2 = level counters)
  * Unknown name -> HM_EINVAL. */

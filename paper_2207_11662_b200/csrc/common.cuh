@@ -86,7 +86,7 @@ struct Params {
     int bfs_words = 64;
     int bfs_heavy = 256;
     int bfs_blocks_per_sm = 0;
-    int bfs_chg_smem = 1;
+    int bfs_chg_smem = 0;      // 1: stage the change bitmaps in shared memory each level; 0: read them via L1
     int bfs_prune = 1;         // exact 2-core pruning of the largest component before the MS-BFS
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
