@@ -18,7 +18,8 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC",
     "-I", os.path.join(ROOT, "include"),
-] + (["-DHM_MSBFS_PROF"] if os.environ.get("HM_MSBFS_PROF") else [])
+] + (["-DHM_MSBFS_PROF"] if os.environ.get("HM_MSBFS_PROF") else []) + \
+    [f"-D{d}" for d in os.environ.get("HM_DEFINES", "").split() if d]
 
 
 def sources():

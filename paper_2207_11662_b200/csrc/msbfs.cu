@@ -151,7 +151,9 @@ __device__ __forceinline__ void or_row(ulonglong2 (&r)[VEC], const ulonglong2 (&
 __device__ __forceinline__ ulonglong2 ld2p(const uint64_t *p, uint64_t pol) {
     if (!pol) return ld2(p);
     ulonglong2 v;
-    asm volatile("ld.global.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+    // gathered rows are random and read once per SM: do not let them evict the bitmaps from L1
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ void st2p(uint64_t *p, ulonglong2 v, uint64_t pol) {
