@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     __shared__ Smem<BLOCK / 32> sm;
     __shared__ unsigned long long s_pl[WT ? BFS_T_BITS : 1][WT ? W : 1];   // T bit planes of the batch window
     __shared__ int s_nb;
+#ifdef HM_MSBFS_PROF
+    __shared__ int s_tmin, s_tmax;
+#endif
     __shared__ ulonglong2 s_red[TPB][T];
     extern __shared__ uint4 s_dyn[];
 
@@ -333,6 +336,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
             __syncthreads();
             PROF_MARK(pf, 0);
+#ifdef HM_MSBFS_PROF
+            const long long t_lvl0 = clock64();
+            if (threadIdx.x == 0) {
+                s_tmin = 0x7fffffff;
+                s_tmax = 0;
+            }
+            __syncthreads();
+#endif
             bool any = false;
 
             // ---- heavy rows: one CTA per row, neighbour list split over teams
@@ -613,8 +624,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 }
                 PROF_MARK(pf, 2);
             }
+#ifdef HM_MSBFS_PROF
+            if (pf.on && lane == 0) {          // spread of the warps' exit times from the unit loop
+                const int te = (int)((clock64() - t_lvl0) >> 4);
+                atomicMin(&s_tmin, te);
+                atomicMax(&s_tmax, te);
+            }
+#endif
             // one flag write per CTA (same-address stores from every group serialise in L2)
             if (__syncthreads_or(any) && threadIdx.x == 0) a.flags[d % 3] = 1;
+#ifdef HM_MSBFS_PROF
+            if (pf.on && threadIdx.x == 0 && a.dbgc) {
+                atomicAdd(a.dbgc + 8202, (unsigned long long)s_tmin << 4);
+                atomicAdd(a.dbgc + 8203, (unsigned long long)s_tmax << 4);
+                atomicAdd(a.dbgc + 8204, 1ull);
+            }
+#endif
             PROF_MARK(pf, 6);
             grid.sync();
             PROF_MARK(pf, 7);

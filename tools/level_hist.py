@@ -46,3 +46,6 @@ if ph.sum() > 0:
     print(f"  per warp: rounds {rounds / nwarps:.0f}, gather iterations {iters / nwarps:.0f}; "
           f"cycles per round {ph[5] / max(rounds, 1):.0f}, "
           f"per level-step per warp {ph.sum() / nwarps / max(cnt[a.level] if a.level else cnt.sum(), 1):.0f}")
+    if dc[8204]:
+        print(f"  per CTA-level: first warp leaves the unit loop at {dc[8202] / dc[8204]:.0f} cycles, "
+              f"last at {dc[8203] / dc[8204]:.0f} cycles ({dc[8204]} CTA-levels)")
