@@ -59,10 +59,6 @@ __global__ void k_keys_to_csr(const uint64_t *__restrict__ k, int64_t nnz, int32
     }
 }
 
-__global__ void k_fill(int32_t *p, int64_t n, int32_t v) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
-}
-
 __device__ __forceinline__ bool bsearch_row(const int32_t *__restrict__ col, int lo, int hi, int v) {
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;

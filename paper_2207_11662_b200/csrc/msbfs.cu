@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     const uint64_t pol_n = (a.hints & 4) ? policy_evict_last() : (a.hints & 8) ? policy_evict_first() : pol_d;
     Prof pf;
     PROF_INIT(pf);
+    (void)pf;
 
     for (int64_t base = 0; base < n_giant; base += B) {
         if (a.nshards > 1 && (int)((base / B) % a.nshards) != a.shard) continue;   // another shard's batch
