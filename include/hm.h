@@ -73,7 +73,8 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)
  *   "bfs_chg_smem": 1 stages the per-level change bitmaps in shared memory, 0 (default) reads them via L1
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
- *   "bfs_dbg"     : debug bits (1 = per-thread fence before grid barriers, 2 = level counters)
+ *   "bfs_dbg"     : debug: bit 1 (value 2) = per-level counters and times (hm_debug_counts);
+ *                   bits 8.. = the one level to profile in HM_MSBFS_PROF builds
  * Unknown name -> HM_EINVAL. */
 hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value);
 
@@ -229,10 +230,11 @@ typedef struct {
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
 
-/* Debug: copy the per-level counters of the last MS-BFS launch made with
- * hm_set_param("bfs_dbg", 2): out[d] = rows changed at level d, out[4096+d] =
- * CTAs that saw level d's change flag set.  n <= 8192 uint64 (host).  ESTATE
- * if no such launch happened. */
+/* Debug: copy the counters of the last MS-BFS launch made with
+ * hm_set_param("bfs_dbg", 2): out[d] = source batches that ran level d,
+ * out[4096+d] = nanoseconds spent in level d (summed over batches), and in
+ * HM_MSBFS_PROF builds out[8192..8204] = per-phase warp cycles and counts.
+ * n <= 335872 uint64 (host).  ESTATE if no such launch happened. */
 hm_status hm_debug_counts(hm_ctx *ctx, uint64_t *out, int32_t n);
 
 #ifdef __cplusplus
