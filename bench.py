@@ -224,13 +224,59 @@ def run_ours(args, rank, world, local_rank):
     value, total_ms = job_value(share * args.steps, total_ms, device=f"cuda:{dev}")
     ms_per_step = total_ms / args.steps
 
+    # ---- per-phase breakdown of one extra (untimed-for-value) step, CUDA events on the ctx stream:
+    # SURVEY §8(d) / PAPER.md:373 accounting: Psi per layer, AND, ground-truth closeness, Theta (CC1, CC2)
+    breakdown = None
+    if not args.shard and not args.fused:
+        ev = []
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            ev.append((name, e))
+
+        flush_l2()
+        torch.cuda.synchronize()
+        mark("start")
+        for i in range(len(h.layers)):
+            ctx.closeness(i, out={})
+            mark(f"psi_L{i}")
+        for T in h.subsets:
+            tag = "".join(map(str, T))
+            g = ctx.and_aggregate(list(T))
+            mark(f"and_{tag}")
+            ctx.closeness(g, out={})
+            mark(f"gt_closeness_{tag}")
+            ctx.topk_closeness(g, K, out=ids_dev)
+            mark(f"gt_topk_{tag}")
+            ctx.compose("cc2", list(T), K, out=ids_dev)
+            mark(f"theta_cc2_{tag}")
+            ctx.compose("cc1", list(T), K, out=ids_dev)
+            mark(f"theta_cc1_{tag}")
+            ctx.compose("naive", list(T), K, out=ids_dev)
+            mark(f"theta_naive_{tag}")
+            ctx.free_graph(g)
+        torch.cuda.synchronize()
+        breakdown = {n: ev[i - 1][1].elapsed_time(e) for i, (n, e) in enumerate(ev) if i > 0}
+        psi_ms = [breakdown[f"psi_L{i}"] for i in range(len(h.layers))]
+        T0 = "".join(map(str, h.subsets[0]))
+        breakdown["sum_psi"] = float(sum(psi_ms))
+        breakdown["max_psi"] = float(max(psi_ms))
+        # the paper's accounting: t_dt = max(Psi) + Theta, t_gt = AND + CC (first subset)
+        breakdown["t_dt_cc1"] = breakdown["max_psi"] + breakdown[f"theta_cc1_{T0}"]
+        breakdown["t_dt_cc2"] = breakdown["max_psi"] + breakdown[f"theta_cc2_{T0}"]
+        breakdown["t_gt"] = breakdown[f"and_{T0}"] + breakdown[f"gt_closeness_{T0}"] + breakdown[f"gt_topk_{T0}"]
+        breakdown = {k: round(v, 4) for k, v in breakdown.items()}
+        ctx.stats(reset=True)
+
     # ---- e2e: host edge lists -> public API -> host results, copies inside the timed region
     e2e = None
     if not args.no_e2e:
         h2d = sum(int(t.numel()) * 4 for t in host_layers)
         d2h = 0
         e_ms = []
-        for it in range(max(1, args.steps)):
+        n_warm = 1                                          # one untimed e2e pass (first-use allocations)
+        for it in range(n_warm + max(1, args.steps)):
             flush_l2()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -249,7 +295,8 @@ def run_ours(args, rank, world, local_rank):
                 ctx.free_graph(g)
             e1.record(s)
             e1.synchronize()
-            e_ms.append(e0.elapsed_time(e1))
+            if it >= n_warm:
+                e_ms.append(e0.elapsed_time(e1))
             d2h = sum(int(o.nbytes) for o in outs)
         e2e_ms = float(np.mean(e_ms))
         e2e_val, e2e_ms = job_value(share, e2e_ms, device=f"cuda:{dev}")
@@ -297,6 +344,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"batch-shard{world}+nccl-allreduce(S)" if args.shard else f"replicas{world}"},
         "s_per_homln": ms_per_step / 1e3,
         "e2e": e2e, "roofline": roof, "clocks": clocks, "gpu_launches": int(round(launches_per_step)),
+        "breakdown_ms": breakdown,
     }
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(h, args.cpu_seconds)
