@@ -124,7 +124,9 @@ hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
  * Also caches, for hm_compose / hm_topk_closeness / hm_cc_nodes: degrees, the
  * mean closeness mu = (correctly rounded sum of c) / V and the CC-node set
  * CH = {v : c(v) > mu}.  Any output pointer may be NULL; each
- * is host or device, length V.  Re-running on a graph recomputes. */
+ * is host or device, length V.  Re-running on a graph recomputes.  With
+ * "bfs_prune" on (default) the call synchronises the context stream once, to
+ * decide whether the exact 2-core pruning of the largest component pays. */
 hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
                        double *closeness, uint64_t *pen_sum);
 
