@@ -57,9 +57,16 @@ namespace cg = cooperative_groups;
 namespace hm {
 namespace {
 
-// threads per CTA (2 CTAs per SM): 512 for plain sums; the weighted kernel (pruned graphs)
-// keeps more live state and runs best with 384 (85 registers instead of 64, no spills)
-constexpr int BLOCK_PLAIN = 512, BLOCK_WEIGHTED = 384;
+// threads per CTA (2 CTAs per SM), measured: the plain kernel runs best at 448 (512: 2.7 %
+// slower, 416: much slower); the weighted kernel (pruned graphs) keeps more live state and
+// runs best at 384 (85 registers, no spills)
+#ifndef HM_BLOCK_PLAIN
+#define HM_BLOCK_PLAIN 448      // measured best for the plain kernel (2 CTAs x 14 warps, 73 registers)
+#endif
+#ifndef HM_BLOCK_WEIGHTED
+#define HM_BLOCK_WEIGHTED 384   // weighted (pruned) kernel: 85 registers, no spills
+#endif
+constexpr int BLOCK_PLAIN = HM_BLOCK_PLAIN, BLOCK_WEIGHTED = HM_BLOCK_WEIGHTED;
 constexpr int CAP = 256;            // staged pairs per warp
 constexpr int SCAN_U = 4;           // arc chunks (of 32) loaded per scan step
 constexpr unsigned FULL = 0xffffffffu;
