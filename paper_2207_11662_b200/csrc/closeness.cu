@@ -162,6 +162,15 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
     }
 }
 
+// upper bound on the MS-BFS rows: vertices with an edge that were not peeled
+__global__ void k_count_rows(const int32_t *row_ptr, const int32_t *rem, int V, int32_t *out) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const bool live = row_ptr[v + 1] > row_ptr[v] && !(rem && rem[v]);
+        const unsigned b = __ballot_sync(__activemask(), live);
+        if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && b) atomicAdd(out, __popc(b));
+    }
+}
+
 // hanging-tree size T of every BFS row (weights of the pruned MS-BFS)
 __global__ void k_row_T(const int32_t *new_to_old, const uint32_t *tsz, const int32_t *scalars, uint32_t *T) {
     const int n_live = scalars[0];
@@ -432,8 +441,24 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     }
     // 4. MS-BFS
     const size_t rowb = (size_t)W * 8;
+    // frontier rows only for vertices that can be BFS rows (an edge, not peeled): large sparse
+    // graphs (many isolated vertices) need far less than V rows of state
+    int64_t frows = V;
+    {
+        Buf cntb(16, s);
+        HM_CUDA(cudaMemsetAsync(cntb.p, 0, 16, s));
+        k_count_rows<<<gb, TB, 0, s>>>(U.rp, rem, V, cntb.as<int32_t>());
+        check_launch("k_count_rows");
+        count_launch(ctx);
+        int32_t h_rows = 0;
+        HM_CUDA(cudaMemcpyAsync(&h_rows, cntb.p, 4, cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        frows = (int64_t)h_rows + 32;
+        if (frows > V) frows = V;
+        if (frows < 32) frows = 32;
+    }
     const size_t bmw = (((size_t)(V + 31) / 32) + 4) & ~(size_t)3;   // multiple of 4 words (16-B rows for uint4 copies)
-    Buf F0((size_t)V * rowb, s), F1((size_t)V * rowb, s), F2((size_t)V * rowb, s);
+    Buf F0((size_t)frows * rowb, s), F1((size_t)frows * rowb, s), F2((size_t)frows * rowb, s);
     Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), Kb((size_t)V * 2 + 16, s), flags(128, s);
     HM_CUDA(cudaMemsetAsync(Srel.p, 0, Srel.bytes, s));
     HM_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, s));

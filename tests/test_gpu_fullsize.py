@@ -145,12 +145,12 @@ def test_fullsize_config(Context, name):
 
 
 def test_large_vertex_count(Context):
-    """Vertex ids near the top of the supported range (V = 2^24 + 7, 16.8 M vertices,
-    mostly isolated): 64-bit state-row offsets (V x 512 B = 8.6 GB per frontier array),
-    the relabelling and the pruning paths.  A random forest plus cycles on 300 K scattered
+    """The top of the supported range, V = 2^26 - 1 (67 M vertices, mostly isolated; R2 in
+    DESIGN.md): 64-bit offsets, the relabelling of 67 M keys, the pruning paths, and frontier
+    state sized by the vertices that can be BFS rows rather than by V.  A random forest plus cycles on 300 K scattered
     vertices (many components, long hanging trees) and one 4097-vertex path; sampled
     vertices checked with the oracle's plain BFS, isolated vertices by definition."""
-    V = (1 << 24) + 7
+    V = (1 << 26) - 1
     rng = np.random.default_rng(24)
     verts = rng.choice(V, size=300_000, replace=False).astype(np.int64)
     E = []
