@@ -227,6 +227,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- per-phase breakdown of one extra (untimed-for-value) step, CUDA events on the ctx stream:
     # SURVEY §8(d) / PAPER.md:373 accounting: Psi per layer, AND, ground-truth closeness, Theta (CC1, CC2)
     breakdown = None
+    accuracy = None
     if not args.shard and not args.fused:
         ev = []
 
@@ -255,6 +256,15 @@ def run_ours(args, rank, world, local_rank):
             mark(f"theta_cc1_{tag}")
             ctx.compose("naive", list(T), K, out=ids_dev)
             mark(f"theta_naive_{tag}")
+            if T == h.subsets[0]:
+                # the paper's evaluation (Table 2): each heuristic's top-K against the
+                # ground-truth top-K, on the library's set-metrics kernel (after the timed marks)
+                gt_ids = ctx.topk_closeness(g, K)
+                accuracy = {}
+                for heur in ("cc1", "cc2", "naive"):
+                    est, _ = ctx.compose(heur, list(T), K)
+                    m = ctx.set_metrics(V, est, gt_ids)
+                    accuracy[heur] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in m.items()}
             ctx.free_graph(g)
         torch.cuda.synchronize()
         breakdown = {n: ev[i - 1][1].elapsed_time(e) for i, (n, e) in enumerate(ev) if i > 0}
@@ -345,6 +355,7 @@ def run_ours(args, rank, world, local_rank):
         "s_per_homln": ms_per_step / 1e3,
         "e2e": e2e, "roofline": roof, "clocks": clocks, "gpu_launches": int(round(launches_per_step)),
         "breakdown_ms": breakdown,
+        "accuracy_vs_gt_topk": accuracy,
     }
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(h, args.cpu_seconds)
