@@ -357,7 +357,7 @@ def run_ours(args, rank, world, local_rank):
         "breakdown_ms": breakdown,
         "accuracy_vs_gt_topk": accuracy,
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:      # the oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(h, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
