@@ -216,6 +216,8 @@ def run_ours(args, rank, world, local_rank):
         e1.record(s)
         times.append((e0, e1))
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     clocks = clk.stop()
     ms = [a.elapsed_time(b) for a, b in times]
     st = ctx.stats(reset=True)
