@@ -362,3 +362,59 @@ def test_sharded_closeness(hm, name, V):
         for g in gids:
             tot = ctx.closeness_partial(g, 0, 2) + ctx.closeness_partial(g, 1, 2)
             assert tot.tolist() == full[g]["S"].tolist()
+
+
+# ---------------------------------------------------------------------------
+# Randomised sweep: graph shapes x every tuning knob (results never depend on them)
+# ---------------------------------------------------------------------------
+def _shape(rng, t):
+    """seeded test graphs with the structures that stress different paths: ER / R-MAT
+    (hubs -> heavy rows), forests with a few cycles (deep hanging trees -> pruning),
+    disjoint pieces of different size (component batching)."""
+    V = rng.choice([2, 3, 7, 31, 32, 33, 100, 257, 700, 1500, 3000])
+    kind = rng.choice(["er", "rmat", "forest", "pieces"])
+    if kind in ("er", "rmat"):
+        m = rng.choice([V // 2, V, 2 * V, 5 * V])
+        return V, {tuple(e) for e in random_graph(V, max(m, 1), seed=5000 + t, kind=kind).tolist()}
+    E = set()
+    if kind == "forest":
+        for v in range(1, V):
+            if rng.random() < 0.95:
+                u = rng.randrange(v)
+                E.add((u, v))
+        for _ in range(rng.randrange(0, max(1, V // 10))):
+            a, b = rng.sample(range(V), 2)
+            E.add((min(a, b), max(a, b)))
+        return V, E
+    start = 0
+    while start < V - 1:                         # pieces: paths, cycles, cliques of random sizes
+        n = min(V - start, rng.choice([2, 3, 5, 17, 64, 200]))
+        shape = rng.choice(["path", "cycle", "clique"])
+        vs = list(range(start, start + n))
+        if shape == "clique" and n <= 17:
+            E |= {(a, b) for i, a in enumerate(vs) for b in vs[i + 1:]}
+        else:
+            E |= {(vs[i], vs[i + 1]) for i in range(n - 1)}
+            if shape == "cycle" and n > 2:
+                E.add((vs[0], vs[-1]))
+        start += n + rng.choice([0, 1, 3])
+    return V, E
+
+
+def test_random_sweep_all_knobs(hm):
+    rng = random.Random(20220722)
+    knobs = dict(bfs_words=[8, 16, 32, 64], bfs_prune=[0, 1], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
+                 bfs_chg_smem=[0, 1], bfs_unit=[8, 16, 32], bfs_heavy=[2, 16, 256], bfs_blocks_per_sm=[0, 1])
+    with hm() as ctx:
+        for t in range(200):
+            V, E = _shape(rng, t)
+            res = O.analyze(V, E)
+            for k, vals in knobs.items():
+                ctx.set_param(k, rng.choice(vals))
+            ctx.load_layers(V, [edges_arr(E)])
+            check_psi(V, E, ctx.closeness(0), res)
+            if t % 6 == 0 and V >= 3:                 # sharded path, same knobs
+                n = rng.choice([2, 3])
+                tot = sum(ctx.closeness_partial(0, r, n).astype(np.uint64) for r in range(n))
+                ctx.closeness_combine(0, tot)
+                check_psi(V, E, ctx.closeness_results(0), res)
