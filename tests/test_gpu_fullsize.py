@@ -76,11 +76,15 @@ def edges_of(rp, col):
     return src[keep] * V + col[keep]
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
-def test_fullsize_config(Context, name):
+@pytest.mark.parametrize("name,knobs", [("C1", {}), ("C2", {}), ("C3", {}), ("C4", {}), ("C5", {}),
+                                        ("C4", {"bfs_prune": 0, "bfs_interleave": 0, "bfs_words": 32})],
+                         ids=["C1", "C2", "C3", "C4", "C5", "C4-noprune-w32"])
+def test_fullsize_config(Context, name, knobs):
     h = build_config(name)
     V, K = h.V, h.K
     with Context() as ctx:
+        for k, v in knobs.items():
+            ctx.set_param(k, v)
         ctx.load_layers(V, h.layers)
         res = []
         for i, L in enumerate(h.layers):
