@@ -67,9 +67,12 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_prune"   : 1 (default) exact 2-core pruning of the largest component before the MS-BFS
  *                   (hanging trees restored by weights and re-rooting; results unchanged), 0 off
  *   "bfs_interleave": 1 (default) CTAs own interleaved light-path units, 0 contiguous ranges
+ *   "bfs_fbar": 0 MS-BFS levels end in the cooperative grid barrier plus an any-change
+ *              flag; 1 (default) one counter atomic per CTA carries both (arrival and "row changed")
  *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
- *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16 or 8)
+ *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16, 8, 4 or 2; 0 = default: chosen from
+ *                   the live rows per warp of the grid, 32 on C5-sized graphs)
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)
  *   "bfs_chg_smem": 1 stages the per-level change bitmaps in shared memory, 0 (default) reads them via L1
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)

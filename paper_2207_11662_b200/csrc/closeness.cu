@@ -10,6 +10,7 @@
 //   5. finalize in original order: S, k, Wasserman-Faust closeness, n-penalty
 //      sum, degree;
 //   6. mu = RN(exact sum c) / V (exactsum.cu) and CH = {v : c(v) > mu}.
+#include <cmath>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -496,10 +497,27 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.nshards = nshards;
     a.interleave = ctx->params.bfs_interleave;
     a.dbg_level = ctx->params.bfs_dbg >> 8;                   // bfs_dbg bits 8.. (profiling builds)
-    a.unit_shift = ctx->params.bfs_unit == 8 ? 2 : ctx->params.bfs_unit == 16 ? 1 : 0;
+    {
+        // rows per work unit: bfs_unit, or (0, auto) about a quarter of the live rows per warp of
+        // a full grid (2 CTAs x 14 warps per SM), as a power of two in [2, 32], 16 taken as 32.
+        // Small graphs need small units to occupy the grid; C5-sized graphs the whole 32-row
+        // groups (unit sweep over C1..C5)
+        int unit = ctx->params.bfs_unit;
+        if (unit <= 0) {
+            const double q = (double)(frows - 32) / ((double)ctx->num_sms * 28.0) / 4.0;
+            const int e = q > 1.0 ? (int)std::lround(std::log2(q)) : 0;
+            unit = 1 << (e < 1 ? 1 : e > 5 ? 5 : e);
+            if (unit == 16) unit = 32;
+        }
+        int us = 0;
+        while ((32 >> us) > unit && us < 4) ++us;     // 32 >> us rows per unit
+        a.unit_shift = us;
+    }
     a.chg_smem = (ctx->params.bfs_chg_smem && bmw * 4 * 2 <= 80 * 1024) ? 1 : 0;
     a.S = Srel.as<uint64_t>();
     a.flags = flags.as<int32_t>();
+    // fused level barrier: two zeroed counters in the same (zeroed) 128-B flags block
+    a.lbar = ctx->params.bfs_fbar ? (unsigned long long *)((char *)flags.p + 64) : nullptr;
     a.counters = ctx->dstats.as<unsigned long long>();
     a.dbgc = nullptr;
     if (ctx->params.bfs_dbg & 2) {

@@ -89,8 +89,9 @@ struct Params {
     int bfs_chg_smem = 0;      // 1: stage the change bitmaps in shared memory each level; 0: read them via L1
     int bfs_prune = 1;         // exact 2-core pruning of the largest component before the MS-BFS
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
+    int bfs_fbar = 1;          // MS-BFS level barrier with the any-change flag folded in
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
-    int bfs_unit = 32;         // MS-BFS light-path rows per work unit (32, 16, 8)
+    int bfs_unit = 0;          // MS-BFS light-path rows per work unit (0 = auto by rows per warp; 32 ... 2)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level
     int timing = 0;

@@ -132,13 +132,16 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         ctx->params.bfs_blocks_per_sm = (int)value;
     } else if (n == "bfs_prune") {
         ctx->params.bfs_prune = value ? 1 : 0;
+    } else if (n == "bfs_fbar") {
+        ctx->params.bfs_fbar = value ? 1 : 0;
     } else if (n == "bfs_interleave") {
         ctx->params.bfs_interleave = value ? 1 : 0;
     } else if (n == "bfs_hints") {
         HM_REQUIRE(value >= 0 && value <= 31, HM_EINVAL, "bfs_hints must be in [0, 31]");
         ctx->params.bfs_hints = (int)value;
     } else if (n == "bfs_unit") {
-        HM_REQUIRE(value == 8 || value == 16 || value == 32, HM_EINVAL, "bfs_unit must be 8, 16 or 32");
+        HM_REQUIRE(value == 0 || value == 2 || value == 4 || value == 8 || value == 16 || value == 32, HM_EINVAL,
+                   "bfs_unit must be 0 (auto), 2, 4, 8, 16 or 32");
         ctx->params.bfs_unit = (int)value;
     } else if (n == "bfs_gd") {
         HM_REQUIRE(value == 0 || value == 2 || value == 4 || value == 8, HM_EINVAL, "bfs_gd must be 0, 2, 4 or 8");

@@ -141,6 +141,7 @@ struct Smem {
     int hi;
     int next;                       // next group to claim in this CTA's range
     int flag;
+    unsigned lb[4];              // fused level barrier (thread 0): expected arrivals, seen any-counts per parity
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
     int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     Prof pf;
     PROF_INIT(pf);
     (void)pf;
+    if (threadIdx.x < 4) sm.lb[threadIdx.x] = 0u;
 
     for (int64_t base = 0; base < n_giant; base += B) {
         if (a.nshards > 1 && (int)((base / B) % a.nshards) != a.shard) continue;   // another shard's batch
@@ -646,7 +648,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
 #endif
             // one flag write per CTA (same-address stores from every group serialise in L2)
-            if (__syncthreads_or(any) && threadIdx.x == 0) a.flags[d % 3] = 1;
+            const int any_cta = __syncthreads_or(any);
+            if (any_cta && threadIdx.x == 0 && !a.lbar) a.flags[d % 3] = 1;
 #ifdef HM_MSBFS_PROF
             if (pf.on && threadIdx.x == 0 && a.dbgc) {
                 atomicAdd(a.dbgc + 8202, (unsigned long long)s_tmin << 4);
@@ -655,10 +658,38 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
 #endif
             PROF_MARK(pf, 6);
-            grid.sync();
+            if (a.lbar) {
+                // level barrier with the any-change flag folded in: each CTA adds
+                // 1 | any << 32 to the level parity's counter; the barrier is complete at
+                // grid arrivals, and the high word grew iff some CTA saw a change.  (The
+                // next arrival on this parity needs every CTA past the next level, so the
+                // value read here is final for level d.)
+                if (threadIdx.x == 0) {
+                    const int p = d & 1;
+                    const unsigned long long add = 1ull | ((unsigned long long)(any_cta ? 1u : 0u) << 32);
+                    __threadfence();
+                    atomicAdd(a.lbar + p, add);
+                    // arrivals expected on this parity: grid x (its levels so far)
+                    const unsigned expect = sm.lb[p] + gridDim.x;
+                    sm.lb[p] = expect;
+                    unsigned long long v;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.lbar + p) : "memory");
+                        if ((int)((unsigned)(v & 0xffffffffull) - expect) >= 0) break;
+                        __nanosleep(20);
+                    }
+                    const unsigned hiw = (unsigned)(v >> 32);
+                    sm.flag = (hiw != sm.lb[2 + p]) ? 1 : 0;
+                    sm.lb[2 + p] = hiw;
+                    __threadfence();
+                }
+                __syncthreads();
+            } else {
+                grid.sync();
+                if (threadIdx.x == 0) sm.flag = *((volatile int32_t *)(a.flags + (d % 3)));
+                __syncthreads();
+            }
             PROF_MARK(pf, 7);
-            if (threadIdx.x == 0) sm.flag = *((volatile int32_t *)(a.flags + (d % 3)));
-            __syncthreads();
             const int fv = sm.flag;
             if (a.dbgc && gtid == 0) {
                 unsigned long long now;

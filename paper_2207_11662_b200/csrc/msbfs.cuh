@@ -31,14 +31,15 @@ struct BfsArgs {
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
-    int unit_shift;
+    int unit_shift;              // light-path work unit = 32 >> unit_shift rows of a 32-row group
     int shard, nshards;          // run batches i = shard, shard + nshards, ... only
-    int interleave;
+    int interleave;              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
     const uint32_t *tw;          // pruned MS-BFS: hanging-tree size T per row (nullptr: unweighted)
-    unsigned long long *planes;  // [BFS_T_BITS][W] scratch: T bit planes of the batch window              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
-    int hints;
-    int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
-                                 // 4 F_d stores evict_last, 8 F_d stores evict_first              // light-path work unit = 32 >> unit_shift rows of a 32-row group
+    unsigned long long *planes;  // [BFS_T_BITS][W] scratch: T bit planes of the batch window
+    int hints;                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
+                                 // 4 F_d stores evict_last, 8 F_d stores evict_first, 16 evict_normal
+    unsigned long long *lbar;    // [2] fused level-barrier counters (zeroed); nullptr: grid.sync + flag
+    int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per

@@ -77,9 +77,10 @@ def test_psi_special(hm, name, V, E):
     E = {(min(u, v), max(u, v)) for u, v in E if u != v}
     res = O.analyze(V, E)
     # narrow batches (B = 512: several batches per component), other team widths and occupancies
-    for words, team, bps, unit, prune in ((8, 0, 0, 8, 1), (16, 4, 0, 16, 0), (64, 32, 1, 32, 1), (64, 16, 1, 8, 0),
-                                          (32, 16, 1, 32, 1)):
+    for words, team, bps, unit, prune, fbar in ((8, 0, 0, 8, 1, 1), (16, 4, 0, 16, 0, 0), (64, 32, 1, 32, 1, 0),
+                                                (64, 16, 1, 4, 0, 1), (32, 16, 1, 2, 1, 1), (64, 16, 0, 8, 1, 1)):
         with hm() as ctx:
+            ctx.set_param("bfs_fbar", fbar)
             ctx.set_param("bfs_prune", prune)
             ctx.set_param("bfs_words", words)
             ctx.set_param("bfs_unit", unit)
@@ -120,8 +121,9 @@ def test_tuning_invariance(hm):
     for words in (8, 16, 32, 64):
         for heavy in (4, 64, 100000):
             for bps in (0, 1):
-                for chg_smem, unit, inter, prune in ((0, 32, 0, 0), (1, 8, 1, 1)):
+                for chg_smem, unit, inter, prune, fbar in ((0, 32, 0, 0, 1), (1, 8, 1, 1, 0), (0, 2, 1, 1, 1)):
                     with hm() as ctx:
+                        ctx.set_param("bfs_fbar", fbar)
                         ctx.set_param("bfs_prune", prune)
                         ctx.set_param("bfs_interleave", inter)
                         ctx.set_param("bfs_unit", unit)
@@ -404,7 +406,8 @@ def _shape(rng, t):
 def test_random_sweep_all_knobs(hm):
     rng = random.Random(20220722)
     knobs = dict(bfs_words=[8, 16, 32, 64], bfs_prune=[0, 1], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
-                 bfs_chg_smem=[0, 1], bfs_unit=[8, 16, 32], bfs_heavy=[2, 16, 256], bfs_blocks_per_sm=[0, 1])
+                 bfs_chg_smem=[0, 1], bfs_unit=[0, 2, 4, 8, 16, 32], bfs_heavy=[2, 16, 256], bfs_blocks_per_sm=[0, 1],
+                 bfs_fbar=[0, 1])
     with hm() as ctx:
         for t in range(200):
             V, E = _shape(rng, t)
