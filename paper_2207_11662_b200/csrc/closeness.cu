@@ -163,6 +163,18 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
     }
 }
 
+// items per heavy row (in place of the prefix the MS-BFS kernel reads): ceil(deg / BFS_HEAVY_CHUNK)
+__global__ void k_heavy_items(const int32_t *heavy, const int32_t *nrp, int n_heavy, int32_t *items) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h <= n_heavy; h += gridDim.x * blockDim.x) {
+        int n = 0;
+        if (h < n_heavy) {
+            const int v = heavy[h];
+            n = (nrp[v + 1] - nrp[v] + BFS_HEAVY_CHUNK - 1) / BFS_HEAVY_CHUNK;
+        }
+        items[h] = n;
+    }
+}
+
 // upper bound on the MS-BFS rows: vertices with an edge that were not peeled
 __global__ void k_count_rows(const int32_t *row_ptr, const int32_t *rem, int V, int32_t *out) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
@@ -445,6 +457,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // frontier rows only for vertices that can be BFS rows (an edge, not peeled): large sparse
     // graphs (many isolated vertices) need far less than V rows of state
     int64_t frows = V;
+    int32_t h_heavy = 0;
     {
         Buf cntb(16, s);
         HM_CUDA(cudaMemsetAsync(cntb.p, 0, 16, s));
@@ -453,6 +466,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         count_launch(ctx);
         int32_t h_rows = 0;
         HM_CUDA(cudaMemcpyAsync(&h_rows, cntb.p, 4, cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaMemcpyAsync(&h_heavy, scalars + 3, 4, cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
         frows = (int64_t)h_rows + 32;
         if (frows > V) frows = V;
@@ -472,6 +486,31 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.scalars = scalars;
     a.heavy = heavy.as<int32_t>();
     a.heavy_deg = heavy_deg;
+    // heavy-row work items: ceil(deg / BFS_HEAVY_CHUNK) per heavy row, their prefix, and the
+    // partial-row accumulators of rows with several items
+    Buf hstart, hacc, hcnt;
+    a.hstart = nullptr;
+    a.hacc = nullptr;
+    a.hcnt = nullptr;
+    if (h_heavy > 0) {
+        hstart.alloc((size_t)(h_heavy + 1) * 4, s);
+        hacc.alloc((size_t)h_heavy * W * 8, s);
+        hcnt.alloc((size_t)h_heavy * 4, s);
+        HM_CUDA(cudaMemsetAsync(hacc.p, 0, hacc.bytes, s));
+        HM_CUDA(cudaMemsetAsync(hcnt.p, 0, hcnt.bytes, s));
+        k_heavy_items<<<grid_for(h_heavy + 1, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(
+            heavy.as<int32_t>(), nrp.as<int32_t>(), h_heavy, hstart.as<int32_t>());
+        check_launch("k_heavy_items");
+        count_launch(ctx);
+        size_t tb = 0;
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, hstart.as<int32_t>(), hstart.as<int32_t>(), h_heavy + 1, s));
+        Buf tmp(tb, s);
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, hstart.as<int32_t>(), hstart.as<int32_t>(), h_heavy + 1, s));
+        count_launch(ctx, 2);
+        a.hstart = hstart.as<int32_t>();
+        a.hacc = hacc.as<unsigned long long>();
+        a.hcnt = hcnt.as<int32_t>();
+    }
     a.F[0] = F0.as<uint64_t>();
     a.F[1] = F1.as<uint64_t>();
     a.F[2] = F2.as<uint64_t>();

@@ -69,6 +69,13 @@ def special_graphs():
     for n in (1024, 1025, 2047, 2049):
         gs.append((f"path-{n}", n, {(i, i + 1) for i in range(n - 1)}))
     gs.append(("tree-3000", 3000, {(i, (i - 1) // 2) for i in range(1, 3000)}))
+    # hubs of degree 1100..3300 inside a sparse random core: heavy rows of 2-4 work items
+    # (BFS_HEAVY_CHUNK = 1024 arcs) that stay unpeeled and change over several levels
+    rng = random.Random(11662)
+    E = {(rng.randrange(4000), rng.randrange(4000)) for _ in range(6000)}
+    for h, deg in ((0, 3300), (1, 2100), (2, 1100), (3, 1025)):
+        E |= {(h, u) for u in rng.sample(range(4, 4000), deg)}
+    gs.append(("hubs-4000", 4000, E))
     return gs
 
 
