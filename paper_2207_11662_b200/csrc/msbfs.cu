@@ -147,8 +147,6 @@ struct Smem {
     int next;                       // next group to claim in this CTA's range
     int flag;
     unsigned lb[4];              // fused level barrier (thread 0): expected arrivals, seen any-counts per parity
-    int hh;                         // heavy row of the current heavy item
-    int hlast;                      // this CTA completed the heavy row (last chunk to arrive)
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
     int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
@@ -218,7 +216,7 @@ template <int W, int BLOCK, bool WT>
 __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                          const int2 *__restrict__ cinfo, const int32_t *__restrict__ heavy,
                                          const int32_t *__restrict__ hstart, unsigned long long *hacc, int32_t *hcnt,
-                                         uint32_t *done, uint16_t *K, uint64_t *S, int &sm_hh, int &sm_hlast, ulonglong2 *s_red_,
+                                         uint32_t *done, uint16_t *K, uint64_t *S, ulonglong2 *s_red_,
                                  const unsigned long long *s_pl_, int s_nb, int n_items, int n_heavy,
                                  int hi, int n_giant, int64_t base, int d, const uint32_t *chp_s,
                                  const uint32_t *chpp_s, const uint64_t *__restrict__ Fc,
@@ -232,6 +230,8 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
     const int tbase = lane - tl;
     const unsigned tmask = ((T == 32) ? FULL : ((1u << T) - 1u)) << tbase;
     bool any = false;
+    __shared__ int sm_hh;               // heavy row of the current item
+    __shared__ int sm_hlast;            // this CTA completed the heavy row (last item to arrive)
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         if (threadIdx.x == 0) {
             int lo = 0, hi2 = n_heavy - 1;                       // last h with hstart[h] <= it
@@ -360,7 +360,8 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
 // W words per row, TL lanes per light row, GD gathers in flight per lane, MINB CTAs per SM
 // WT: weighted sums for the pruned component (prune.cu): S(v) += d * sum over the new
 // sources s of (1 + T(s)), the T sum taken from per-batch bit planes of T in shared memory
-template <int W, int TL, int GD, int MINB, bool WT, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
+// HV: heavy-row path compiled in (false only for graphs without heavy rows: a leaner kernel)
+template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2;           // lanes per row in the heavy path
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
@@ -520,9 +521,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             // ---- heavy rows: items of BFS_HEAVY_CHUNK arcs (hstart: first item of each heavy row)
             // dealt round-robin over the CTAs, each item's arcs split over the CTA's teams.  A row
             // of several items ORs its partial rows into hacc; the last item to arrive commits.
-            if (n_items > 0)
+            if (HV && n_items > 0)
                 any = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
-                                                a.K, a.S, sm.hh, sm.hlast, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
+                                                a.K, a.S, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
                                                 hi, n_giant, base, d, chp_s, chpp_s, Fc, Fp, Fn, chn);
             PROF_MARK(pf, 1);
 
@@ -824,7 +825,14 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         HM_MSBFS_CASE(32, 16, 8, 1)
         HM_MSBFS_CASE(32, 8, 2, 2)
         HM_MSBFS_CASE(64, 32, 4, 2)
-        HM_MSBFS_CASE(64, 16, 2, 2)
+    case ((64 * 100 + 16) * 100 + 2 * 10 + 2):                 // default: lean variants without heavy rows
+        if (a.hstart)
+            kern = a.tw ? (const void *)msbfs_kernel<64, 16, 2, 2, true> : (const void *)msbfs_kernel<64, 16, 2, 2, false>;
+        else
+            kern = a.tw ? (const void *)msbfs_kernel<64, 16, 2, 2, true, false>
+                        : (const void *)msbfs_kernel<64, 16, 2, 2, false, false>;
+        block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
+        break;
         HM_MSBFS_CASE(64, 16, 4, 1)
         HM_MSBFS_CASE(64, 16, 8, 1)
         HM_MSBFS_CASE(64, 32, 8, 1)
