@@ -573,6 +573,11 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cudaEventRecord(e0, s));
     }
     const int grid = launch_msbfs(W, ctx->params.bfs_team, ctx->params.bfs_gd, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
+    if (grid == -1)                     // no instantiation for this (words, team, gathers, CTAs/SM)
+        throw Error(HM_EINVAL, "no MS-BFS kernel for bfs_words=" + std::to_string(W) + " bfs_team=" +
+                                   std::to_string(ctx->params.bfs_team) + " bfs_gd=" + std::to_string(ctx->params.bfs_gd) +
+                                   " bfs_blocks_per_sm=" + std::to_string(ctx->params.bfs_blocks_per_sm) +
+                                   " (see launch_msbfs in msbfs.cu for the built combinations)");
     if (grid < 0) {
         cudaGetLastError();
         throw Error(HM_ECUDA, "msbfs launch failed (" + std::to_string(grid) + ")");

@@ -174,7 +174,20 @@ def test_errors(hm):
             ctx.topk_closeness(0, 6)
         with pytest.raises(HmError, match="HM_ESTATE"):
             ctx.free_graph(0)
+        # tuning knobs: out-of-range values, and a combination with no compiled kernel
+        for name, bad in (("bfs_words", 7), ("bfs_unit", 3), ("bfs_unit", 64), ("bfs_gd", 3), ("bfs_team", 2)):
+            with pytest.raises(HmError, match="HM_EINVAL"):
+                ctx.set_param(name, bad)
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.set_param("no_such_knob", 1)
+        ctx.set_param("bfs_team", 8)
+        ctx.set_param("bfs_gd", 4)
+        with pytest.raises(HmError, match="HM_EINVAL.*no MS-BFS kernel"):
+            ctx.closeness(1)
+        ctx.set_param("bfs_team", 0)
+        ctx.set_param("bfs_gd", 0)
         # context stays usable after errors
+        ctx.closeness(1)
         g = ctx.and_aggregate([0, 1])
         assert ctx.graph_info(g) == (5, 1)
 
