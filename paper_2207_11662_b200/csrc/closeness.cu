@@ -492,10 +492,11 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.hstart = nullptr;
     a.hacc = nullptr;
     a.hcnt = nullptr;
+    a.hclaim = nullptr;
     if (h_heavy > 0) {
         hstart.alloc((size_t)(h_heavy + 1) * 4, s);
         hacc.alloc((size_t)h_heavy * W * 8, s);
-        hcnt.alloc((size_t)h_heavy * 4, s);
+        hcnt.alloc((size_t)h_heavy * 4 + 16, s);
         HM_CUDA(cudaMemsetAsync(hacc.p, 0, hacc.bytes, s));
         HM_CUDA(cudaMemsetAsync(hcnt.p, 0, hcnt.bytes, s));
         k_heavy_items<<<grid_for(h_heavy + 1, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(
@@ -510,6 +511,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         a.hstart = hstart.as<int32_t>();
         a.hacc = hacc.as<unsigned long long>();
         a.hcnt = hcnt.as<int32_t>();
+        a.hclaim = a.hcnt + h_heavy;    // 3 claim counters after the per-row item counts (zeroed)
     }
     a.F[0] = F0.as<uint64_t>();
     a.F[1] = F1.as<uint64_t>();

@@ -136,8 +136,11 @@ struct Prof {
 #define PROF_FLUSH(p, dst) do { } while (0)
 #endif
 
+#ifndef HM_HEAVY_DYN
+#define HM_HEAVY_DYN 1          // heavy items: 0 dealt before the light units, 1 claimed after them
+#endif
 #ifndef HM_HEAVY_GD
-#define HM_HEAVY_GD 4
+#define HM_HEAVY_GD 8
 #endif
 constexpr int HGD = HM_HEAVY_GD;    // heavy-row gathers in flight per team
 
@@ -209,14 +212,14 @@ __device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglon
 }
 
 // Heavy rows (degree > heavy_deg), out of line: items of BFS_HEAVY_CHUNK arcs (hstart: first item
-// of each heavy row) dealt round-robin over the CTAs, each item's arcs split over the CTA's teams
-// of T = W/2 lanes.  A row of several items ORs its partial rows into hacc; the last item to
+// of each heavy row), claimed from the level's counter hclaim (nullptr: dealt round-robin over the
+// CTAs), each item's arcs split over the CTA's teams of T = W/2 lanes.  A row of several items ORs its partial rows into hacc; the last item to
 // arrive commits.  Returns whether this thread committed a change.
 template <int W, int BLOCK, bool WT>
 __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                          const int2 *__restrict__ cinfo, const int32_t *__restrict__ heavy,
                                          const int32_t *__restrict__ hstart, unsigned long long *hacc, int32_t *hcnt,
-                                         uint32_t *done, uint16_t *K, uint64_t *S, ulonglong2 *s_red_,
+                                         uint32_t *done, uint16_t *K, uint64_t *S, int32_t *hclaim, ulonglong2 *s_red_,
                                  const unsigned long long *s_pl_, int s_nb, int n_items, int n_heavy,
                                  int hi, int n_giant, int64_t base, int d, const uint32_t *chp_s,
                                  const uint32_t *chpp_s, const uint64_t *__restrict__ Fc,
@@ -232,8 +235,11 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
     bool any = false;
     __shared__ int sm_hh;               // heavy row of the current item
     __shared__ int sm_hlast;            // this CTA completed the heavy row (last item to arrive)
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    __shared__ int sm_it;               // claimed item (hclaim: dynamic claims)
+    for (int it_s = blockIdx.x;; it_s += gridDim.x) {
         if (threadIdx.x == 0) {
+            const int it = hclaim ? atomicAdd(hclaim, 1) : it_s;
+            sm_it = it;
             int lo = 0, hi2 = n_heavy - 1;                       // last h with hstart[h] <= it
             while (lo < hi2) {
                 const int mid = (lo + hi2 + 1) >> 1;
@@ -242,6 +248,8 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
             sm_hh = lo;
         }
         __syncthreads();
+        const int it = sm_it;
+        if (it >= n_items) break;                                // block-uniform
         const int h = sm_hh;
         const int v = heavy[h];
         const int i0 = hstart[h], nch = hstart[h + 1] - i0;
@@ -451,6 +459,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
         }
         if (gtid == 0) a.flags[1] = 0;
+        if (HV && gtid == 0 && a.hclaim) a.hclaim[1] = 0;        // level 1's heavy-item claims
         if constexpr (WT) {
             // bit planes of T over the giant's source window: plane b, word w, bit j =
             // bit b of T(row base + 64 w + j) (rows outside [0, n_giant) weigh 1: T = 0)
@@ -489,6 +498,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             uint32_t *chz = a.chg[(d + 1) & 3];
             for (int64_t w = gtid; w < ngroups; w += nthreads) chz[w] = 0u;
             if (gtid == 0) a.flags[(d + 1) % 3] = 0;
+            if (HV && gtid == 0 && a.hclaim) a.hclaim[(d + 1) % 3] = 0;   // next level's claims
             // stage the two previous change bitmaps in shared memory
             const uint32_t *chp_s = chp, *chpp_s = chpp;
             if (threadIdx.x == 0)
@@ -518,12 +528,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 #endif
             bool any = false;
 
-            // ---- heavy rows: items of BFS_HEAVY_CHUNK arcs (hstart: first item of each heavy row)
-            // dealt round-robin over the CTAs, each item's arcs split over the CTA's teams.  A row
-            // of several items ORs its partial rows into hacc; the last item to arrive commits.
-            if (HV && n_items > 0)
+            // ---- heavy rows (heavy_items): items of BFS_HEAVY_CHUNK arcs, claimed after the light
+            // units (below); HM_HEAVY_DYN 0 deals them round-robin here instead
+            if (HV && !HM_HEAVY_DYN && n_items > 0)
                 any = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
-                                                a.K, a.S, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
+                                                a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
                                                 hi, n_giant, base, d, chp_s, chpp_s, Fc, Fp, Fn, chn);
             PROF_MARK(pf, 1);
 
@@ -735,6 +744,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 atomicMax(&s_tmax, te);
             }
 #endif
+            // heavy items claimed dynamically by the CTAs as they finish their light units (a CTA
+            // holding a hub no longer finishes last; C4 layers -5 %, C3 -6 % against dealing them
+            // round-robin before the light units; compiling both placements in is slower than either)
+            if (HV && HM_HEAVY_DYN && n_items > 0)
+                any |= heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
+                                                 a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
+                                                 n_heavy, hi, n_giant, base, d, chp_s, chpp_s, Fc, Fp, Fn, chn);
             // one flag write per CTA (same-address stores from every group serialise in L2)
             const int any_cta = __syncthreads_or(any);
             if (any_cta && threadIdx.x == 0 && !a.lbar) a.flags[d % 3] = 1;

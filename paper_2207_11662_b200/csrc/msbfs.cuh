@@ -8,7 +8,10 @@ namespace hm {
 // Rows of degree > min(heavy_deg, BFS_MAX_LIGHT_DEG) are processed by whole CTAs.
 constexpr int BFS_MAX_LIGHT_DEG = 1 << 30;
 constexpr int BFS_T_BITS = 24;
-constexpr int BFS_HEAVY_CHUNK = 1024;   // arcs per heavy-row work item (one CTA each)        // pruned MS-BFS: hanging-tree sizes T < 2^24 (weight bit planes)
+#ifndef HM_HEAVY_CHUNK
+#define HM_HEAVY_CHUNK 1024
+#endif
+constexpr int BFS_HEAVY_CHUNK = HM_HEAVY_CHUNK;   // arcs per heavy-row work item (one CTA each)        // pruned MS-BFS: hanging-tree sizes T < 2^24 (weight bit planes)
 
 // Device-resident description of one relabelled graph for the MS-BFS kernel.
 // Rows 0..n_live-1 are the non-isolated vertices, grouped by connected
@@ -24,6 +27,7 @@ struct BfsArgs {
     const int32_t *hstart;       // [n_heavy + 1] first item of each heavy row (ceil(deg / BFS_HEAVY_CHUNK) items)
     unsigned long long *hacc;    // [n_heavy][W] zeroed: partial OR rows of multi-item heavy rows
     int32_t *hcnt;               // [n_heavy] zeroed: items of the row done this level
+    int32_t *hclaim;             // [3] heavy-item claim counters, rotated by level
     int32_t heavy_deg;
     uint64_t *F[3];              // [n_live][W] frontier rows of levels d, d-1, d-2 (rotating)
     uint32_t *chg[4];            // row bitmaps "changed at level", rotating over 4 levels
