@@ -61,7 +61,8 @@ const char *hm_last_error(const hm_ctx *ctx);
 
 /* Tuning knobs (results never depend on them):
  *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16, 32 or 64; sources per batch = 64*words)
- *   "bfs_heavy"   : degree above which a row is processed by a whole CTA
+ *   "bfs_heavy"   : degree above which a row goes to the MS-BFS heavy path (work items of 1024 arcs
+ *                   claimed by whole CTAs); 0 = default: 256, or 64 on graphs of average degree < 8
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (1, or 0 / 2 = two)
  *   "bfs_gd"      : MS-BFS neighbour-row gathers in flight per lane (0 = default, 2, 4, 8)
  *   "bfs_prune"   : 1 (default) exact 2-core pruning of the largest component before the MS-BFS

@@ -436,7 +436,12 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         count_launch(ctx, 4 + 3 * 4 + 2);   // our kernels + CUB passes (approximate)
     }
     // 3. relabelled CSR + heavy list (rows heavier than the MS-BFS light path takes)
-    const int heavy_deg = ctx->params.bfs_heavy < BFS_MAX_LIGHT_DEG ? ctx->params.bfs_heavy : BFS_MAX_LIGHT_DEG;
+    // heavy-row threshold: bfs_heavy, or (0, auto) 256 on graphs of average degree >= 8 and 64 on
+    // sparser ones, where a row of a few dozen arcs already stalls its warp's lock-step rounds
+    // (heavy sweep over C2-C4 layers and AND graphs)
+    int heavy_param = ctx->params.bfs_heavy;
+    if (heavy_param <= 0) heavy_param = (U.nnz >= (int64_t)8 * V) ? 256 : 64;
+    const int heavy_deg = heavy_param < BFS_MAX_LIGHT_DEG ? heavy_param : BFS_MAX_LIGHT_DEG;
     k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
                                      n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
                                      heavy.as<int32_t>(), scalars, heavy_deg, rem, V);

@@ -84,7 +84,7 @@ struct Graph {
 
 struct Params {
     int bfs_words = 64;
-    int bfs_heavy = 256;
+    int bfs_heavy = 0;         // MS-BFS heavy-row degree threshold (0 = auto: 256, or 64 below average degree 8)
     int bfs_blocks_per_sm = 0;
     int bfs_chg_smem = 0;      // 1: stage the change bitmaps in shared memory each level; 0: read them via L1
     int bfs_prune = 1;         // exact 2-core pruning of the largest component before the MS-BFS

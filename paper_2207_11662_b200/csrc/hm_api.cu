@@ -125,7 +125,7 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
                    "bfs_words must be 8, 16, 32 or 64");
         ctx->params.bfs_words = (int)value;
     } else if (n == "bfs_heavy") {
-        HM_REQUIRE(value >= 1, HM_EINVAL, "bfs_heavy must be >= 1");
+        HM_REQUIRE(value >= 0, HM_EINVAL, "bfs_heavy must be >= 0 (0 = automatic)");
         ctx->params.bfs_heavy = (int)value;
     } else if (n == "bfs_blocks_per_sm") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_blocks_per_sm must be 0 (= 2), 1 or 2");
