@@ -126,6 +126,19 @@ namespace hm {
 
 inline void count_launch(hm_ctx *ctx, int n = 1) { ctx->stats.launches += n; }
 
+// Row of arc j of a CSR (row_ptr[0..V], V >= 1, 0 <= j < row_ptr[V]): the largest u with
+// row_ptr[u] <= j.  Arc-parallel kernels use it so that a hub row is spread over many threads
+// instead of serialising one warp (R-MAT hubs of 5-8 K arcs).
+__device__ __forceinline__ int csr_row_of(const int32_t *__restrict__ row_ptr, int V, int64_t j) {
+    int lo = 0, hi = V - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (row_ptr[mid] <= j) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 inline void check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(HM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));

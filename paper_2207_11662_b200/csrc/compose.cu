@@ -79,49 +79,45 @@ __device__ __forceinline__ bool bsearch_row(const int32_t *__restrict__ col, int
     return false;
 }
 
-// CC1 main loop (pseudocode PAPER.md:486-507, flat r-ary, Z7-Z12): warp per
-// common CC node u.  I = ∩_i {v ∈ NBD_i(u) : ratio_i(v) < avgAND}; if |I| > 1
-// add I; always add u.  R is a bitmap (atomicOr -- set union is order-free).
-__global__ void k_cc1_main(LayerPtrs L, int V, const double *ratio, const double *avg_and_p, uint32_t *R) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// CC1 main loop (pseudocode PAPER.md:486-507, flat r-ary, Z7-Z12), arc-parallel over the
+// arcs (u, v) of layer 0 (the intersection is symmetric in the layers, so any layer can drive;
+// CC nodes are often hubs, whose rows would serialise a warp):
+//   v ∈ I(u) iff ratio_i(v) < avgAND and v ∈ NBD_i(u) for every layer i.
+// pass 0 counts |I(u)| (warp-aggregated per row); pass 1 adds I(u) when |I(u)| > 1 and adds
+// every common u.  R is a bitmap (atomicOr -- set union is order-free).
+__device__ __forceinline__ bool cc1_common(const LayerPtrs &L, int u) {
+    bool common = true;
+    for (int i = 0; i < L.r; ++i) common = common && ((L.ch[i][u >> 5] >> (u & 31)) & 1u);
+    return common;
+}
+__global__ void k_cc1_main(LayerPtrs L, int V, int64_t nnz0, const double *ratio, const double *avg_and_p,
+                           int32_t *icnt, uint32_t *R, int pass) {
     const double avg_and = *avg_and_p;
-    for (int64_t u = w0; u < V; u += nw) {
-        bool common = true;
-        for (int i = 0; i < L.r; ++i) common = common && ((L.ch[i][u >> 5] >> (u & 31)) & 1u);
-        if (!common) continue;
-        // driver: the layer with the shortest row u
-        int drv = 0, best = 0x7fffffff;
-        for (int i = 0; i < L.r; ++i) {
-            const int d = L.rp[i][u + 1] - L.rp[i][u];
-            if (d < best) { best = d; drv = i; }
-        }
-        const int rb = L.rp[drv][u], re = L.rp[drv][u + 1];
-        int cnt = 0;
-        // pass 1: count |I|
-        for (int j = rb + lane; j < re; j += 32) {
-            const int v = L.cl[drv][j];
-            bool in = true;
-            for (int i = 0; i < L.r && in; ++i) {
-                in = ratio[(size_t)i * V + v] < avg_and;
-                if (in && i != drv) in = bsearch_row(L.cl[i], L.rp[i][u], L.rp[i][u + 1], v);
-            }
-            cnt += in ? 1 : 0;
-        }
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (cnt > 1) {
-            for (int j = rb + lane; j < re; j += 32) {
-                const int v = L.cl[drv][j];
-                bool in = true;
+    const int64_t n = nnz0 > V ? nnz0 : V;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        if (pass == 1 && j < V && cc1_common(L, (int)j)) atomicOr(&R[j >> 5], 1u << (j & 31));
+        bool in = false;
+        int u = -1;
+        if (j < nnz0) {
+            u = csr_row_of(L.rp[0], V, j);
+            if (cc1_common(L, u) && (pass == 0 || icnt[u] > 1)) {
+                const int v = L.cl[0][j];
+                in = true;
                 for (int i = 0; i < L.r && in; ++i) {
                     in = ratio[(size_t)i * V + v] < avg_and;
-                    if (in && i != drv) in = bsearch_row(L.cl[i], L.rp[i][u], L.rp[i][u + 1], v);
+                    if (in && i != 0) in = bsearch_row(L.cl[i], L.rp[i][u], L.rp[i][u + 1], v);
                 }
-                if (in) atomicOr(&R[v >> 5], 1u << (v & 31));
+                if (in && pass == 1) atomicOr(&R[v >> 5], 1u << (v & 31));
             }
         }
-        if (lane == 0) atomicOr(&R[u >> 5], 1u << (u & 31));
+        if (pass == 0) {
+            const unsigned act = __activemask();
+            const unsigned inm = __ballot_sync(act, in);
+            if (in) {
+                const unsigned same = __match_any_sync(inm, u);
+                if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(icnt + u, __popc(same));
+            }
+        }
     }
 }
 
@@ -300,11 +296,17 @@ void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t
                 exact_mean(ctx, ratio.as<double>() + (size_t)i * V, V, fin.as<uint8_t>(), avgs.as<double>() + i,
                            nullptr);
             k_cc1_avgand<<<1, 32, 0, s>>>(avgs.as<double>(), r, avgs.as<double>() + r);
-            k_cc1_main<<<gw, TB, 0, s>>>(L, V, ratio.as<double>(), avgs.as<double>() + r, R.as<uint32_t>());
+            Buf icnt((size_t)V * 4, s);
+            HM_CUDA(cudaMemsetAsync(icnt.p, 0, icnt.bytes, s));
+            const int64_t nnz0 = gs[0]->nnz;
+            const unsigned ga = grid_for(nnz0 > V ? nnz0 : (int64_t)V, TB, (int64_t)ctx->num_sms * 16);
+            for (int pass = 0; pass < 2; ++pass)
+                k_cc1_main<<<ga, TB, 0, s>>>(L, V, nnz0, ratio.as<double>(), avgs.as<double>() + r,
+                                             icnt.as<int32_t>(), R.as<uint32_t>(), pass);
             k_cc1_keys<<<g, TB, 0, s>>>(L, V, R.as<uint32_t>(), mindeg.as<int32_t>(), keys.as<uint64_t>(),
                                        cnt.as<int32_t>());
             check_launch("cc1");
-            count_launch(ctx, 3);
+            count_launch(ctx, 4);
         }
         int32_t nR = 0;
         HM_CUDA(cudaMemcpyAsync(&nR, cnt.p, 4, cudaMemcpyDeviceToHost, s));

@@ -77,49 +77,33 @@ struct AggIn {
     int drv;   // driver graph (fewest arcs)
 };
 
-// AND pass 1: per driver arc, membership in every other graph's (sorted) row; row counts.
-__global__ void k_and_count(AggIn in, int32_t V, uint8_t *keep, int32_t *rowcnt) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// AND pass 1 (arc-parallel): keep[j] = 1 iff driver arc j = (u, v) is in every other graph's
+// sorted row u
+__global__ void k_and_keep(AggIn in, int32_t V, int64_t nd, int32_t *keep) {
     const int32_t *rpd = in.rp[in.drv];
     const int32_t *cld = in.cl[in.drv];
-    for (int64_t u = w0; u < V; u += nw) {
-        const int rb = rpd[u], re = rpd[u + 1];
-        int cnt = 0;
-        for (int j = rb + lane; j < re; j += 32) {
-            const int v = cld[j];
-            bool ok = true;
-            for (int g = 0; g < in.r && ok; ++g) {
-                if (g == in.drv) continue;
-                ok = bsearch_row(in.cl[g], in.rp[g][u], in.rp[g][u + 1], v);
-            }
-            keep[j] = ok ? 1 : 0;
-            cnt += ok ? 1 : 0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += (int64_t)gridDim.x * blockDim.x) {
+        const int u = csr_row_of(rpd, V, j);
+        const int v = cld[j];
+        bool ok = true;
+        for (int g = 0; g < in.r && ok; ++g) {
+            if (g == in.drv) continue;
+            ok = bsearch_row(in.cl[g], in.rp[g][u], in.rp[g][u + 1], v);
         }
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) rowcnt[u] = cnt;
+        keep[j] = ok ? 1 : 0;
     }
 }
 
-// AND pass 2: ordered compaction of kept driver arcs into the output CSR
-__global__ void k_and_fill(AggIn in, int32_t V, const uint8_t *__restrict__ keep, const int32_t *__restrict__ orp,
-                           int32_t *ocol) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// AND pass 2: kept arcs to their exclusive-scan positions (CSR order is arc order), and
+// row_ptr[u] = pos[first driver arc of u]
+__global__ void k_and_fill(AggIn in, int32_t V, int64_t nd, const int32_t *__restrict__ keep,
+                           const int32_t *__restrict__ pos, int32_t *orp, int32_t *ocol) {
     const int32_t *rpd = in.rp[in.drv];
     const int32_t *cld = in.cl[in.drv];
-    for (int64_t u = w0; u < V; u += nw) {
-        const int rb = rpd[u], re = rpd[u + 1];
-        int out = orp[u];
-        for (int j0 = rb; j0 < re; j0 += 32) {
-            const int j = j0 + lane;
-            const bool k = j < re && keep[j];
-            const unsigned b = __ballot_sync(0xffffffffu, k);
-            if (k) ocol[out + __popc(b & ((1u << lane) - 1u))] = cld[j];
-            out += __popc(b);
-        }
+    const int64_t n = nd > (int64_t)V + 1 ? nd : (int64_t)V + 1;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        if (j < nd && keep[j]) ocol[pos[j]] = cld[j];
+        if (j <= V) orp[j] = pos[rpd[j]];
     }
 }
 
@@ -240,23 +224,25 @@ void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, 
     const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
     if (is_and) {
         const int64_t nd = in[a.drv]->nnz;
-        Buf keep((size_t)(nd > 0 ? nd : 1), s), cnt((size_t)(V + 1) * 4, s);
-        Buf orp((size_t)(V + 1) * 4, s);
-        HM_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, s));
-        k_and_count<<<gw, TB, 0, s>>>(a, V, keep.as<uint8_t>(), cnt.as<int32_t>());
+        HM_REQUIRE(nd < (int64_t)INT32_MAX, HM_ERANGE, "AND aggregate too large for an int32 CSR");
+        // keep flags (+ a zero sentinel at nd), their exclusive scan = output positions
+        Buf keep((size_t)(nd + 1) * 4, s), pos((size_t)(nd + 1) * 4, s), orp((size_t)(V + 1) * 4, s);
+        HM_CUDA(cudaMemsetAsync(keep.as<int32_t>() + nd, 0, 4, s));
+        const unsigned ga = grid_for(nd > V ? nd : (int64_t)V + 1, TB, (int64_t)ctx->num_sms * 16);
+        if (nd > 0) k_and_keep<<<ga, TB, 0, s>>>(a, V, nd, keep.as<int32_t>());
         size_t tb = 0;
-        HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int32_t>(), orp.as<int32_t>(), V + 1, s));
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), nd + 1, s));
         Buf tmp(tb, s);
-        HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int32_t>(), orp.as<int32_t>(), V + 1, s));
+        HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, keep.as<int32_t>(), pos.as<int32_t>(), nd + 1, s));
         int32_t nnz = 0;
-        HM_CUDA(cudaMemcpyAsync(&nnz, orp.as<int32_t>() + V, 4, cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaMemcpyAsync(&nnz, pos.as<int32_t>() + nd, 4, cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
         out.V = V;
         out.nnz = nnz;
-        out.row_ptr = std::move(orp);
         out.col.alloc((size_t)(nnz > 0 ? nnz : 1) * 4, s);
-        if (nnz > 0) k_and_fill<<<gw, TB, 0, s>>>(a, V, keep.as<uint8_t>(), out.row_ptr.as<int32_t>(),
-                                                  out.col.as<int32_t>());
+        k_and_fill<<<ga, TB, 0, s>>>(a, V, nd, keep.as<int32_t>(), pos.as<int32_t>(), orp.as<int32_t>(),
+                                     out.col.as<int32_t>());
+        out.row_ptr = std::move(orp);
         check_launch("and_aggregate");
         count_launch(ctx, 3);
     } else {
