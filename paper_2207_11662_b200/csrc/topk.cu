@@ -11,6 +11,7 @@
 // the digit holding the K-th element.  After 12 passes the exact K-th
 // composite T is known; every element <= T (exactly K) is gathered and sorted
 // in shared memory (bitonic, K <= 4096) -- larger K use a stable device sort.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -19,6 +20,7 @@
 
 namespace hm {
 namespace {
+namespace cg = cooperative_groups;
 
 constexpr int TB = 256;
 constexpr int SORT_MAX = 4096;
@@ -29,6 +31,7 @@ struct SelState {
     int rem;                   // rank still to find inside the current prefix group (1-based)
     unsigned int hist[256];
     int count;                 // gathered elements
+    int done;                  // k_select_coop: the K-th element is fixed early (its key's group fits whole)
 };
 
 // digit p (0..11) of composite (key, id): p < 8 -> key byte (7-p), else id byte (11-p)
@@ -36,26 +39,27 @@ __device__ __forceinline__ unsigned digit_of(uint64_t key, uint32_t id, int p) {
     return p < 8 ? (unsigned)((key >> (8 * (7 - p))) & 0xff) : (unsigned)((id >> (8 * (11 - p))) & 0xff);
 }
 
-__device__ __forceinline__ bool prefix_match(uint64_t key, uint32_t id, const SelState &st, int p) {
+__device__ __forceinline__ bool prefix_match(uint64_t key, uint32_t id, uint64_t pkey, uint32_t pid, int p) {
     // digits 0..p-1 must match
     if (p == 0) return true;
     if (p <= 8) {
         const int sh = 64 - 8 * p;
-        return (sh >= 64) ? true : ((key >> sh) == (st.pkey >> sh));
+        return (sh >= 64) ? true : ((key >> sh) == (pkey >> sh));
     }
-    if (key != st.pkey) return false;
+    if (key != pkey) return false;
     const int sh = 32 - 8 * (p - 8);
-    return (sh >= 32) ? true : ((id >> sh) == (st.pid >> sh));
+    return (sh >= 32) ? true : ((id >> sh) == (pid >> sh));
 }
 
 __global__ void k_hist(const uint64_t *__restrict__ keys, int n, SelState *st, int p) {
     __shared__ unsigned h[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
-    const SelState s = *st;   // prefix (hist part unused here)
+    const uint64_t pkey = st->pkey;
+    const uint32_t pid = st->pid;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
-        if (prefix_match(k, (uint32_t)i, s, p)) atomicAdd(&h[digit_of(k, (uint32_t)i, p)], 1u);
+        if (prefix_match(k, (uint32_t)i, pkey, pid, p)) atomicAdd(&h[digit_of(k, (uint32_t)i, p)], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
@@ -85,6 +89,91 @@ __global__ void k_pick(SelState *st, int p) {
 __global__ void k_gather(const uint64_t *__restrict__ keys, int n, SelState *st, uint64_t *ok, uint32_t *oid) {
     const uint64_t tk = st->pkey;
     const uint32_t ti = st->pid;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (k < tk || (k == tk && (uint32_t)i <= ti)) {
+            const int pos = atomicAdd(&st->count, 1);
+            ok[pos] = k;
+            oid[pos] = (uint32_t)i;
+        }
+    }
+}
+
+// The whole select in one cooperative launch: per pass a block histogram of the digit among the
+// prefix-matching elements, merged into st->hist; after a grid barrier warp 0 of block 0 finds the
+// digit holding the rem-th element (prefix sums over 8 bins per lane) and extends the prefix; after
+// the 12th pass every block gathers its elements <= T.  (The multi-launch path below is kept for
+// grids the cooperative launch cannot place.)
+__global__ void __launch_bounds__(TB) k_select_coop(const uint64_t *__restrict__ keys, int n, SelState *st,
+                                                    uint64_t *ok, uint32_t *oid) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned h[256];
+    __shared__ unsigned long long s_pkey;
+    __shared__ unsigned s_pid;
+    for (int p = 0; p < 12; ++p) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+        if (threadIdx.x == 0) {
+            s_pkey = __ldcg(&st->pkey);
+            s_pid = __ldcg(&st->pid);
+        }
+        __syncthreads();
+        const uint64_t pkey = s_pkey;
+        const uint32_t pid = s_pid;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            const uint64_t k = keys[i];
+            if (prefix_match(k, (uint32_t)i, pkey, pid, p)) atomicAdd(&h[digit_of(k, (uint32_t)i, p)], 1u);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 256; i += blockDim.x)
+            if (h[i]) atomicAdd(&st->hist[i], h[i]);
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = __ldcg(&st->hist[lane * 8 + q]);
+                tot += c[q];
+            }
+            unsigned incl = tot;                         // inclusive prefix over lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int rem = st->rem;
+            const unsigned excl = incl - tot;
+            // the lane whose bins hold the rem-th element: excl < rem <= incl
+            const bool mine = (int)excl < rem && rem <= (int)incl;
+            const unsigned who = __ballot_sync(0xffffffffu, mine);
+            if (mine) {
+                int r = rem - (int)excl;
+                int b = 0;
+                for (; b < 7; ++b) {
+                    if (r <= (int)c[b]) break;
+                    r -= (int)c[b];
+                }
+                const unsigned dg = (unsigned)(lane * 8 + b);
+                st->rem = r;
+                if (p < 8) st->pkey |= (unsigned long long)dg << (8 * (7 - p));
+                else st->pid |= dg << (8 * (11 - p));
+                if (p == 7 && r == (int)c[b]) {              // every element of key T is in: no id passes
+                    st->pid = 0xffffffffu;
+                    st->done = 1;
+                }
+            }
+            if (!who && lane == 0) {                     // unreachable when K <= n
+                if (p < 8) st->pkey |= 255ull << (8 * (7 - p));
+                else st->pid |= 255u << (8 * (11 - p));
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) st->hist[lane * 8 + q] = 0;
+        }
+        grid.sync();
+        if (p == 7 && __ldcg(&st->done)) break;                 // grid-uniform
+    }
+    const uint64_t tk = __ldcg(&st->pkey);
+    const uint32_t ti = __ldcg(&st->pid);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
         if (k < tk || (k == tk && (uint32_t)i <= ti)) {
@@ -171,12 +260,28 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
     SelState *st = stb.as<SelState>();
     HM_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), s));
     k_sel_init<<<1, 32, 0, s>>>(st, K);
-    const unsigned g = grid_for(n, TB, (int64_t)ctx->num_sms * 4);
-    for (int p = 0; p < 12; ++p) {
-        k_hist<<<g, TB, 0, s>>>(d_keys, n, st, p);
-        k_pick<<<1, 32, 0, s>>>(st, p);
+    // one cooperative launch (grid: one CTA per 1 K keys, at most 4 per SM and what fits)
+    int per_sm = 0;
+    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, TB, 0));
+    if (per_sm > 4) per_sm = 4;
+    int gc = (int)grid_for(n, TB * 4, (int64_t)ctx->num_sms * per_sm);
+    if (gc < 1) gc = 1;
+    if (per_sm >= 1) {
+        const uint64_t *kp = d_keys;
+        uint64_t *okp = ok.as<uint64_t>();
+        uint32_t *oip = oid.as<uint32_t>();
+        void *args[] = {(void *)&kp, (void *)&n, (void *)&st, (void *)&okp, (void *)&oip};
+        HM_CUDA(cudaLaunchCooperativeKernel((const void *)k_select_coop, dim3(gc), dim3(TB), args, 0, s));
+        count_launch(ctx, 2);
+    } else {
+        const unsigned g = grid_for(n, TB, (int64_t)ctx->num_sms * 4);
+        for (int p = 0; p < 12; ++p) {
+            k_hist<<<g, TB, 0, s>>>(d_keys, n, st, p);
+            k_pick<<<1, 32, 0, s>>>(st, p);
+        }
+        k_gather<<<g, TB, 0, s>>>(d_keys, n, st, ok.as<uint64_t>(), oid.as<uint32_t>());
+        count_launch(ctx, 25);
     }
-    k_gather<<<g, TB, 0, s>>>(d_keys, n, st, ok.as<uint64_t>(), oid.as<uint32_t>());
     int P = 1;
     while (P < K) P <<= 1;
     const size_t sm = (size_t)P * 12;
@@ -184,7 +289,7 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
         HM_CUDA(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_sort_small<<<1, 1024, sm, s>>>(ok.as<uint64_t>(), oid.as<uint32_t>(), K, P, d_ids_out);
     check_launch("topk");
-    count_launch(ctx, 27);
+    count_launch(ctx, 1);
 }
 
 }  // namespace hm
