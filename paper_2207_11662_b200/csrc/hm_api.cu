@@ -132,6 +132,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         ctx->params.bfs_blocks_per_sm = (int)value;
     } else if (n == "bfs_prune") {
         ctx->params.bfs_prune = value ? 1 : 0;
+    } else if (n == "cc_init") {
+        ctx->params.cc_init = value ? 1 : 0;
     } else if (n == "bfs_fbar") {
         ctx->params.bfs_fbar = value ? 1 : 0;
     } else if (n == "bfs_interleave") {

@@ -5,6 +5,7 @@
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import argparse
+import time
 from paper_2207_11662_b200 import Context
 from synth import build_config
 
@@ -25,10 +26,13 @@ with Context(0) as ctx:
     ctx.closeness(g, out={})
     ctx.sync()
     ctx.stats(reset=True)
+    t0 = time.perf_counter()
     for r in range(a.reps - 1):
         ctx.closeness(g, out={})
     ctx.sync()
+    call_ms = (time.perf_counter() - t0) * 1e3 / max(a.reps - 1, 1)
     st = ctx.stats()
     print(f"{a.config} graph {a.graph} {' '.join(a.set)}: {st['bfs_ms'] / st['bfs_launches']:.2f} ms/launch, "
-          f"levels/launch {st['bfs_levels'] / st['bfs_launches']:.0f}, batches/launch {st['bfs_batches'] / st['bfs_launches']:.0f}",
+          f"levels/launch {st['bfs_levels'] / st['bfs_launches']:.0f}, batches/launch {st['bfs_batches'] / st['bfs_launches']:.0f}, "
+          f"whole closeness call {call_ms:.2f} ms",
           flush=True)
