@@ -72,8 +72,9 @@ const char *hm_last_error(const hm_ctx *ctx);
  *              flag; 1 (default) one counter atomic per CTA carries both (arrival and "row changed")
  *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
- *   "cc_init"     : 1 connected-component union-find starts from parent = smallest
- *                   neighbour; 0 (default) from parent = self
+ *   "cc_init"     : connected components: 2 (default) sampled union-find (unite each vertex with its
+ *                   first 2 neighbours, then only rows outside the most frequent root unite over the
+ *                   rest); 0 union over every arc; 1 as 0 starting from parent = smallest neighbour
  *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16, 8, 4 or 2; 0 = default: chosen from
  *                   the live rows per warp of the grid, 32 on C5-sized graphs)
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)

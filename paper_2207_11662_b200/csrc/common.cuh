@@ -91,7 +91,7 @@ struct Params {
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_fbar = 1;          // MS-BFS level barrier with the any-change flag folded in
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
-    int cc_init = 0;           // 1: union-find starts from parent = smallest neighbour (slower on C3: 4.75 vs 4.4 ms per layer)
+    int cc_init = 2;           // components: 0 union over all arcs, 1 from parent = smallest neighbour, 2 sampled (Afforest)
     int bfs_unit = 0;          // MS-BFS light-path rows per work unit (0 = auto by rows per warp; 32 ... 2)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level

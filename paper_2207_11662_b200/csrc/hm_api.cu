@@ -133,7 +133,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_prune") {
         ctx->params.bfs_prune = value ? 1 : 0;
     } else if (n == "cc_init") {
-        ctx->params.cc_init = value ? 1 : 0;
+        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "cc_init must be 0, 1 or 2");
+        ctx->params.cc_init = (int)value;
     } else if (n == "bfs_fbar") {
         ctx->params.bfs_fbar = value ? 1 : 0;
     } else if (n == "bfs_interleave") {
