@@ -313,7 +313,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms = float(np.mean(e_ms))
         e2e_val, e2e_ms = job_value(share, e2e_ms, device=f"cuda:{dev}")
         e2e = {"value": e2e_val, "unit": "TEPS", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "steps_ms": [round(x, 3) for x in e_ms]}
 
     # ---- roofline of the MS-BFS kernel
     import json as _json
