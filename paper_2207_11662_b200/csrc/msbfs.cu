@@ -27,8 +27,9 @@
 //    (row bitmaps "changed at level d" rotate over 4 levels);
 //  * complete rows are skipped (bitmap `done`).
 //
-// Level step, light rows (one warp per 32-row group, groups claimed
-// dynamically inside a CTA's contiguous range):
+// Level step, light rows (one warp per work unit of 32, 16, 8, 4 or 2 rows of a
+// 32-row group; CTA b owns units b, b + grid, ... and its warps claim them
+// dynamically, starting at the batch's source window):
 //  1. scan: packed arcs (neighbour << 5 | row in group), SCAN_U x 32 at a time,
 //     coalesced; pairs (row, changed neighbour) staged in shared memory in arc
 //     order, hence grouped by row;
@@ -36,14 +37,16 @@
 //     warp's TL-lane teams in lock-step rounds; each row's state and frontier
 //     gathers are issued together (VEC x 16 B per lane per row), OR-ed, committed;
 //  3. the group's chg / done words are published with one atomicOr each.
-// Rows of degree > heavy_deg (R-MAT hubs) are handled by whole CTAs first.
-// The any-change flag of a level is written once per CTA and read once per CTA.
+// Rows of degree > heavy_deg (R-MAT hubs) are cut into items of BFS_HEAVY_CHUNK
+// arcs that whole CTAs claim after their light units (heavy_items, out of line;
+// the last item of a row commits it).  The level barrier is one atomic per CTA on
+// a per-parity counter that also carries the level's any-change count.
 //
 // (tools/experiments/ keeps the variants measured and not kept: two interleaved
 // batch streams with split grid barriers, half-CTA stream parts, a warp-wide
 // pipelined item stream, per-CTA owned rows.)
 //
-// Memory layout: frontier rows are W*8 bytes (256 B at W=32), row-major.
+// Memory layout: frontier rows are W*8 bytes (512 B at the default W=64), row-major.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
