@@ -65,8 +65,9 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   claimed by whole CTAs); 0 = default: 256, or 64 on graphs of average degree < 8
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (1, or 0 / 2 = two)
  *   "bfs_gd"      : MS-BFS neighbour-row gathers in flight per lane (0 = default, 2, 4, 8)
- *   "bfs_prune"   : 1 (default) exact 2-core pruning of the largest component before the MS-BFS
- *                   (hanging trees restored by weights and re-rooting; results unchanged), 0 off
+ *   "bfs_prune"   : exact 2-core pruning of the largest component before the MS-BFS (hanging
+ *                   trees restored by weights and re-rooting; results unchanged): 1 on, 0 off,
+ *                   2 (default) on for V >= 4096
  *   "bfs_interleave": 1 (default) CTAs own interleaved light-path units, 0 contiguous ranges
  *   "bfs_fbar": 0 MS-BFS levels end in the cooperative grid barrier plus an any-change
  *              flag; 1 (default) one counter atomic per CTA carries both (arrival and "row changed")
@@ -132,7 +133,7 @@ hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
  * mean closeness mu = (correctly rounded sum of c) / V and the CC-node set
  * CH = {v : c(v) > mu}.  Any output pointer may be NULL; each
  * is host or device, length V.  Re-running on a graph recomputes.  With
- * "bfs_prune" on (default) the call synchronises the context stream once, to
+ * pruning on ("bfs_prune" 1, or 2 with V >= 4096) the call synchronises the context stream once, to
  * decide whether the exact 2-core pruning of the largest component pays. */
 hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
                        double *closeness, uint64_t *pen_sum);
@@ -154,7 +155,7 @@ hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n);
  * original vertex order, to S_partial (host or device).  The element-wise sum
  * over all nshards shards (e.g. an NCCL all-reduce) is the graph's
  * pre-finalisation sum vector, the same for every nshards (each batch
- * contributes once): S itself when "bfs_prune" is 0, else the pruned core's
+ * contributes once): S itself when pruning is off, else the pruned core's
  * weighted sums (peeled vertices 0).  Only that sum is meaningful, through
  * hm_closeness_combine.
  * hm_closeness_combine finalises graph g from that sum S_total (host or device,

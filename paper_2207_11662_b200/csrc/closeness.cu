@@ -469,7 +469,10 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
 
     // 1b. exact 2-core pruning of the largest component (prune.cu; single graph only)
     Prune pr;
-    if (ctx->params.bfs_prune && gs.size() == 1)
+    // pruning: on (1), off (0), or (2, default) on from V = 4096, below which its kernels and host
+    // round trip cost more than the BFS they save (C1: 0.32 vs 0.26 ms per closeness call)
+    const bool want_prune = ctx->params.bfs_prune == 1 || (ctx->params.bfs_prune == 2 && V >= 4096);
+    if (want_prune && gs.size() == 1)
         prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr);
     const int32_t *rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
 

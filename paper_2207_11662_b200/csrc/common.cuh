@@ -87,7 +87,7 @@ struct Params {
     int bfs_heavy = 0;         // MS-BFS heavy-row degree threshold (0 = auto: 256, or 64 below average degree 8)
     int bfs_blocks_per_sm = 0;
     int bfs_chg_smem = 0;      // 1: stage the change bitmaps in shared memory each level; 0: read them via L1
-    int bfs_prune = 1;         // exact 2-core pruning of the largest component before the MS-BFS
+    int bfs_prune = 2;         // exact 2-core pruning before the MS-BFS: 1 on, 0 off, 2 on from V = 4096
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_fbar = 1;          // MS-BFS level barrier with the any-change flag folded in
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)

@@ -131,7 +131,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_blocks_per_sm must be 0 (= 2), 1 or 2");
         ctx->params.bfs_blocks_per_sm = (int)value;
     } else if (n == "bfs_prune") {
-        ctx->params.bfs_prune = value ? 1 : 0;
+        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_prune must be 0, 1 or 2 (auto)");
+        ctx->params.bfs_prune = (int)value;
     } else if (n == "cc_init") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "cc_init must be 0, 1 or 2");
         ctx->params.cc_init = (int)value;
