@@ -233,8 +233,11 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
 }
 
 // items per heavy row (in place of the prefix the MS-BFS kernel reads): ceil(deg / BFS_HEAVY_CHUNK)
-__global__ void k_heavy_items(const int32_t *heavy, const int32_t *nrp, int n_heavy, int32_t *items) {
-    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h <= n_heavy; h += gridDim.x * blockDim.x) {
+// for h < n_heavy (device count, at most `bound`), 0 for n_heavy <= h <= bound
+__global__ void k_heavy_items(const int32_t *heavy, const int32_t *nrp, const int32_t *n_heavy_dev, int bound,
+                              int32_t *items) {
+    const int n_heavy = min(*n_heavy_dev, bound);
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h <= bound; h += gridDim.x * blockDim.x) {
         int n = 0;
         if (h < n_heavy) {
             const int v = heavy[h];
@@ -547,7 +550,13 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // graphs (many isolated vertices) need far less than V rows of state
     int64_t frows = V;
     int32_t h_heavy = 0;
-    {
+    // small graphs (<= 256 MB of frontier rows at V rows) skip the row count and its host round trip:
+    // F is sized for V rows and the heavy-row arrays for the bound nnz / (heavy_deg + 1)
+    const bool count_rows = (int64_t)V * (int64_t)rowb * 3 > ((int64_t)256 << 20);
+    if (!count_rows) {
+        const int64_t bound = U.nnz / ((int64_t)heavy_deg + 1);
+        h_heavy = (int32_t)(bound < V ? bound : V);
+    } else {
         Buf cntb(16, s);
         HM_CUDA(cudaMemsetAsync(cntb.p, 0, 16, s));
         k_count_rows<<<gb, TB, 0, s>>>(U.rp, rem, V, cntb.as<int32_t>());
@@ -589,7 +598,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cudaMemsetAsync(hacc.p, 0, hacc.bytes, s));
         HM_CUDA(cudaMemsetAsync(hcnt.p, 0, hcnt.bytes, s));
         k_heavy_items<<<grid_for(h_heavy + 1, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(
-            heavy.as<int32_t>(), nrp.as<int32_t>(), h_heavy, hstart.as<int32_t>());
+            heavy.as<int32_t>(), nrp.as<int32_t>(), scalars + 3, h_heavy, hstart.as<int32_t>());
         check_launch("k_heavy_items");
         count_launch(ctx);
         size_t tb = 0;
