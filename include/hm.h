@@ -132,9 +132,11 @@ hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
  * Also caches, for hm_compose / hm_topk_closeness / hm_cc_nodes: degrees, the
  * mean closeness mu = (correctly rounded sum of c) / V and the CC-node set
  * CH = {v : c(v) > mu}.  Any output pointer may be NULL; each
- * is host or device, length V.  Re-running on a graph recomputes.  With
- * pruning on ("bfs_prune" 1, or 2 with V >= 4096) the call synchronises the context stream once, to
- * decide whether the exact 2-core pruning of the largest component pays. */
+ * is host or device, length V.  Re-running on a graph recomputes.  Host round
+ * trips (context-stream synchronisations) inside the call: one with pruning on
+ * ("bfs_prune" 1, or 2 with V >= 4096), to decide whether the exact 2-core
+ * pruning of the largest component pays; one when V * 64 * bfs_words * 3 bytes
+ * exceed 256 MB, to size the frontier rows by the live rows. */
 hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
                        double *closeness, uint64_t *pen_sum);
 
