@@ -135,7 +135,7 @@ hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
  * is host or device, length V.  Re-running on a graph recomputes.  Host round
  * trips (context-stream synchronisations) inside the call: one with pruning on
  * ("bfs_prune" 1, or 2 with V >= 4096), to decide whether the exact 2-core
- * pruning of the largest component pays; one when V * 64 * bfs_words * 3 bytes
+ * pruning of the largest component pays; one when V * 8 * bfs_words * 3 bytes
  * exceed 256 MB, to size the frontier rows by the live rows. */
 hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
                        double *closeness, uint64_t *pen_sum);
