@@ -1,6 +1,8 @@
 """summarise an ncu report: key SOL metrics + top stall lines (sass)"""
 import csv, subprocess, sys, io
 rep = sys.argv[1]
+k_launch = int(sys.argv[2]) if len(sys.argv) > 2 else 0      # which captured launch (0 = first)
+sel = ["--launch-skip", str(k_launch), "--launch-count", "1"] if k_launch else []
 det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(det)))
 hdr = r[0]
@@ -8,23 +10,28 @@ want = ["Duration", "DRAM Throughput", "L2 Cache Throughput", "L1/TEX Cache Thro
         "Executed Ipc Active", "L1/TEX Hit Rate", "L2 Hit Rate", "Memory Throughput", "Warp Cycles Per Issued Instruction",
         "Executed Instructions", "Avg. Active Threads Per Warp", "Registers Per Thread", "Achieved Occupancy",
         "Eligible Warps Per Scheduler", "No Eligible"]
-ids = [dict(zip(hdr, row)).get("ID") for row in r[1:]]
-first = ids[0] if ids else None
+ids = []
+for row in r[1:]:
+    i = dict(zip(hdr, row)).get("ID")
+    if i not in ids:
+        ids.append(i)
+first = ids[k_launch] if len(ids) > k_launch else None
 for row in r[1:]:
     d = dict(zip(hdr, row))
-    if d.get("ID") != first:          # first captured launch only
+    if d.get("ID") != first:          # the selected captured launch only
         continue
     if d.get("Metric Name") in want:
         print(f"  {d['Metric Name']:<40} {d['Metric Value']:>16} {d['Metric Unit']}")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 h2 = rr[0]
-vals = dict(zip(h2, rr[2])) if len(rr) > 2 else {}
+vals = dict(zip(h2, rr[2 + k_launch])) if len(rr) > 2 + k_launch else {}
 units = dict(zip(h2, rr[1])) if len(rr) > 1 else {}
 for k in ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "lts__t_sector_hit_rate.pct", "gpu__time_duration.sum"]:
     if k in vals:
         print(f"  {k:<40} {vals[k]:>16} {units.get(k,'')}")
-sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True, text=True).stdout
+sass = subprocess.run(["ncu", "-i", rep, *sel, "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
+                      text=True).stdout
 rows = list(csv.reader(io.StringIO(sass)))
 hdr = rows[1]
 data = []
