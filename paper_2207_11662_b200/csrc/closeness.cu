@@ -554,6 +554,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // F is sized for V rows and the heavy-row arrays for the bound nnz / (heavy_deg + 1)
     const bool count_rows = (int64_t)V * (int64_t)rowb * 3 > ((int64_t)256 << 20);
     if (!count_rows) {
+        if (frows < 32) frows = 32;                                  // as the counted path
         const int64_t bound = U.nnz / ((int64_t)heavy_deg + 1);
         h_heavy = (int32_t)(bound < V ? bound : V);
     } else {
