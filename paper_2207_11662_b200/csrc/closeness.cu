@@ -143,26 +143,27 @@ __global__ void k_cc_compress(int32_t *p, int32_t *label, int32_t *csize, int V)
     }
 }
 
-// component keys: roots -> ((V - size) << 32 | root); others -> V << 32 (sort last)
-__global__ void k_comp_keys(const int32_t *label, const int32_t *csize, uint64_t *key, int V) {
+// component keys: roots -> ((V - size) << sh | root); others -> V << sh (sort last); sh = bits of V
+__global__ void k_comp_keys(const int32_t *label, const int32_t *csize, uint64_t *key, int V, int sh) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-        key[v] = (label[v] == v) ? (((uint64_t)(V - csize[v]) << 32) | (uint32_t)v)
-                                 : ((uint64_t)V << 32);
+        key[v] = (label[v] == v) ? (((uint64_t)(V - csize[v]) << sh) | (uint32_t)v)
+                                 : ((uint64_t)V << sh);
 }
 
 // sorted component table; scalars[1] = n_giant (if > 1), scalars[2] = n_comp
 __global__ void k_comp_tables(const uint64_t *keys, int32_t *size_s, int32_t *rank_of_root,
-                              int32_t *scalars, int V) {
+                              int32_t *scalars, int V, int sh) {
+    const uint64_t lo = (1ull << sh) - 1ull;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
-        const bool valid = (k >> 32) < (uint64_t)V;
+        const bool valid = (k >> sh) < (uint64_t)V;
         if (valid) {
-            const int sz = V - (int)(k >> 32);
-            const int root = (int)(k & 0xffffffffull);
+            const int sz = V - (int)(k >> sh);
+            const int root = (int)(k & lo);
             size_s[i] = sz;
             rank_of_root[root] = i;
             if (i == 0) scalars[1] = sz > 1 ? sz : 0;
-            const bool last = (i + 1 == V) || ((keys[i + 1] >> 32) >= (uint64_t)V);
+            const bool last = (i + 1 == V) || ((keys[i + 1] >> sh) >= (uint64_t)V);
             if (last) scalars[2] = i + 1;
         } else {
             size_s[i] = 0;
@@ -179,18 +180,18 @@ __global__ void k_nlive(const int32_t *size_s, const int32_t *cstart, int32_t *s
 
 // peeled vertices (rem != nullptr, rem[v] > 0) sort after every component: no BFS row
 __global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, const int32_t *rem, uint64_t *key,
-                            int V) {
+                            int V, int sh) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-        key[v] = ((rem && rem[v]) ? ((uint64_t)V << 32) : ((uint64_t)rank_of_root[label[v]] << 32)) | (uint32_t)v;
+        key[v] = ((rem && rem[v]) ? ((uint64_t)V << sh) : ((uint64_t)rank_of_root[label[v]] << sh)) | (uint32_t)v;
 }
 
 __global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32_t *degl, const int32_t *size_s,
                        const int32_t *cstart, int32_t *new_to_old, int32_t *old_to_new,
-                       int32_t *new_deg, int2 *cinfo, int V) {
+                       int32_t *new_deg, int2 *cinfo, int V, int sh) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
-        const int old = (int)(k & 0xffffffffull);
-        const int r = (int)(k >> 32);
+        const int old = (int)(k & ((1ull << sh) - 1ull));
+        const int r = (int)(k >> sh);
         new_to_old[i] = old;
         old_to_new[old] = i;
         if (r >= V) {                       // peeled vertex: no row
@@ -396,7 +397,9 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     const int W = ctx->params.bfs_words;
     const unsigned gb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
     const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
-    const int end_bit = 32 + nbits((uint64_t)V);
+    // sort keys (high << sh) | vertex with high <= V: sh = bits of V, 2 sh bits sorted
+    const int sh = nbits((uint64_t)V);
+    const int end_bit = 2 * sh;
 
     // per-graph outputs
     for (Graph *g : gs) {
@@ -492,7 +495,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // 2. component order and vertex order
     // (batching by live component sizes: the pruned component counts its core only)
     k_comp_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), pr.active ? pr.lsize.as<int32_t>() : csize.as<int32_t>(),
-                                  key1.as<uint64_t>(), V);
+                                  key1.as<uint64_t>(), V, sh);
     count_launch(ctx);
     {
         size_t tb = 0;
@@ -505,18 +508,18 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
                                                end_bit, s));
         k_comp_tables<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), size_s.as<int32_t>(), rank.as<int32_t>(),
-                                       scalars, V);
+                                       scalars, V, sh);
         size_t tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, size_s.as<int32_t>(), cstart.as<int32_t>(), V, s));
         k_nlive<<<gb, TB, 0, s>>>(size_s.as<int32_t>(), cstart.as<int32_t>(), scalars, V);
-        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem, key1.as<uint64_t>(), V);
+        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem, key1.as<uint64_t>(), V, sh);
         tbs = tb;
         HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tbs, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
                                                end_bit, s));
         k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), U.rp, pr.active ? pr.degl.as<int32_t>() : nullptr,
                                 size_s.as<int32_t>(),
                                 cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
-                                ndeg.as<int32_t>(), cinfo.as<int2>(), V);
+                                ndeg.as<int32_t>(), cinfo.as<int2>(), V, sh);
         tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, ndeg.as<int32_t>(), nrp.as<int32_t>(), V + 1, s));
         check_launch("relabel");
