@@ -287,7 +287,7 @@ def run_ours(args, rank, world, local_rank):
         h2d = sum(int(t.numel()) * 4 for t in host_layers)
         d2h = 0
         e_ms = []
-        n_warm = 1                                          # one untimed e2e pass (first-use allocations)
+        n_warm = 2                                          # untimed e2e passes (first-use allocations, pool growth)
         for it in range(n_warm + max(1, args.steps)):
             flush_l2()
             torch.cuda.synchronize()
