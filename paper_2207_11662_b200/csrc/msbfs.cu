@@ -42,9 +42,9 @@
 // the last item of a row commits it).  The level barrier is one atomic per CTA on
 // a per-parity counter that also carries the level's any-change count.
 //
-// (tools/experiments/ keeps the variants measured and not kept: two interleaved
-// batch streams with split grid barriers, half-CTA stream parts, a warp-wide
-// pipelined item stream, per-CTA owned rows.)
+// (Variants measured and not kept -- two interleaved batch streams with split grid
+// barriers, half-CTA stream parts, a warp-wide pipelined item stream, per-CTA owned
+// rows, a level-1 push step -- are in git history up to commit 93c73e1.)
 //
 // Memory layout: frontier rows are W*8 bytes (512 B at the default W=64), row-major.
 #include <cooperative_groups.h>

@@ -365,6 +365,56 @@ def test_cc1_golden_six_vertex():
     assert O.cc1([r2, r1], 10)[0] == g["CC1_ranked"]
 
 
+def test_cc1_golden_eight_vertex():
+    """Second hand-executed instance: isolated vertices (Z8, Z16),
+    avg_1 != avg_2 with ratios between them (Eq. 3 max), |I| = 1 (Z9), a ratio
+    exactly equal to avgAND (Z11 strict <), est vs est/mindeg ranking (Z13)."""
+    g = json.load(open(os.path.join(GOLDEN, "cc1_eight_vertex.json")))
+    V = g["V"]
+    L1 = O.canonical_edges(V, g["L1"])
+    L2 = O.canonical_edges(V, g["L2"])
+    r1, r2 = layer(V, L1), layer(V, L2)
+    for r, t in ((r1, "1"), (r2, "2")):
+        assert r["S"] == g["S" + t] and r["k"] == g["k" + t] and r["pen"] == g["pen" + t]
+        assert r["deg"] == g["deg" + t]
+        exact = [Fraction(a, b) for a, b in g[f"c{t}_num_den"]]     # c = (k-1)^2 / (S (V-1))
+        assert all(abs(Fraction(x) - e) <= e * Fraction(1, 2**51) for x, e in zip(r["c"], exact))
+        assert sorted(r["CH"]) == g["CH" + t]
+    mindeg, ratios = O.degdist_ratios([r1, r2])
+    assert mindeg == g["mindeg"]
+    for rat, t in ((ratios[0], "1"), (ratios[1], "2")):
+        want = [math.inf if nd is None else float(Fraction(*nd)) for nd in g[f"ratio{t}_num_den"]]
+        assert rat == want
+    ranked, nR, R = O.cc1([r1, r2], V)
+    assert sorted(R) == g["CC1_R"] and nR == len(g["CC1_R"])
+    assert ranked == g["CC1_ranked"]
+    assert O.cc1([r2, r1], V)[0] == g["CC1_ranked"]              # symmetric in layer order
+    assert O.cc1([r1, r2], 2)[0] == g["CC1_ranked"][:2]
+    top, est = O.cc2([r1, r2], 4)
+    assert est == g["CC2_est"] and top == g["CC2_top4"]
+    assert sorted(O.cc2_above_average([r1, r2])) == g["CC2_avg"]
+    A = O.and_aggregate([L1, L2])
+    assert A == O.canonical_edges(V, g["AND_edges"])
+    ra = layer(V, A)
+    assert ra["S"] == g["AND_S"] and ra["pen"] == g["AND_pen"]
+    assert sorted(ra["CH"]) == g["GT_CH"]
+    assert O.topk_closeness(ra["c"], 3) == g["GT_top3"]
+    assert sorted(O.naive([r1, r2], V)[2]) == g["naive"]
+    for u in range(V):
+        assert est[u] <= ra["pen"][u]                               # PAPER.md:546
+
+
+def test_cc2_above_average_strict_on_cycles():
+    """Z4 applied to CC2 ("above average"): identical cycle layers give
+    every vertex the same score (V-1)/est; with V = 8 the fsum mean of 8 equal
+    dyadic scores is exactly that score, so the strict > selects nobody."""
+    for V in (4, 8, 16):
+        r = O.analyze(V, cycle(V))
+        assert r["pen"] == [V * V // 4] * V                          # C_n, n even: S = n^2/4
+        assert O.cc2_above_average([r, r]) == set()
+        assert O.cc2_above_average([r, r, r]) == set()
+
+
 def _three_layers(rng, V, base_p=0.04, keep=0.8, extra=0.004):
     base = rand_graph(rng, V, base_p)
     return [{e for e in base if rng.random() < keep} | rand_graph(rng, V, extra) for _ in range(3)]
