@@ -44,7 +44,7 @@ enum {
     HM_ESTATE = -5    /* unknown / freed graph id, compose before closeness, free of a layer              */
 };
 
-enum { HM_NAIVE = 0, HM_CC1 = 1, HM_CC2 = 2, HM_CC2_AVG = 3 };   /* hm_compose heuristics */
+enum { HM_NAIVE = 0, HM_CC1 = 1, HM_CC2 = 2, HM_CC2_AVG = 3, HM_CC1_RARY = 4 };   /* hm_compose heuristics */
 
 /* ---------------------------------------------------------------- context */
 
@@ -195,16 +195,23 @@ hm_status hm_topk_closeness(hm_ctx *ctx, int32_t g, int32_t K, int32_t *ids_out)
  *   HM_CC2  (Alg. 1): est(v) = max_i pen_i(v); the K
  *           vertices of largest Eq. 1 score (V-1)/est, i.e. smallest (est, id);
  *           writes exactly K ids, *count_out = K.
- *   HM_CC1  (Eq. 2, Eq. 3; pseudocode :477-507; flat r-ary):
- *           result set R, ranked by RN(est/mindeg) ascending then id; writes
- *           min(K, |R|) ids, *count_out = |R|.
+ *   HM_CC1  (Eq. 2, Eq. 3; pseudocode :477-507): the paper
+ *           defines CC1 for a PAIR of layers only, so r must be 2 (r > 2 ->
+ *           HM_EINVAL).  Result set R, ranked by RN(est/mindeg) ascending then
+ *           id; writes min(K, |R|) ids, *count_out = |R|.
+ *   HM_CC1_RARY (explicit opt-in, reading Z12 of DESIGN.md §3): CC1 for any
+ *           2 <= r <= 8 in the flat r-ary form -- mindeg = min_i deg_i,
+ *           avgAND = max_i avg_i, I(u) = the intersection over all r layers
+ *           of the candidate neighbourhoods.  Identical to HM_CC1 when r = 2.
  *   HM_NAIVE: intersection of the CC-node sets, ranked by id;
  *           writes min(K, |R|) ids, *count_out = |R|.
  *   HM_CC2_AVG ("above average" form of CC2): score(v) =
  *           (V-1)/est(v) (Eq. 1, binary64, 0 if est == 0); R = {v : score(v) >
  *           mean score}, the mean being the correctly rounded sum / V; ids
  *           ascending; writes min(K, |R|) ids, *count_out = |R|.
- * 1 <= K <= V.  ids_out host or device; count_out host (may be NULL). */
+ * 1 <= K <= V.  ids_out host or device; count_out host or device (may be NULL).
+ * With device ids_out AND (device or NULL) count_out the call never
+ * synchronises the stream: ids_out receives K entries, those past |R| set to -1. */
 hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, int32_t r,
                      int32_t K, int32_t *ids_out, int32_t *count_out);
 
@@ -218,6 +225,21 @@ hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, i
  * Errors: V <= 0 or n < 0 -> EINVAL; an id outside [0, V) -> ERANGE. */
 hm_status hm_set_metrics(hm_ctx *ctx, int32_t V, const int32_t *est_ids, int64_t n_est,
                          const int32_t *gt_ids, int64_t n_gt, double *out);
+
+/* Exact mean of non-negative doubles, the reducer behind every "average" of
+ * the method: the CC-node threshold "higher than the average",
+ * the layer averages of Eq. 3 and the CC2
+ * above-average threshold.  Reading Z6:
+ * mean = RN(exact sum of the selected x[i]) / count, one IEEE division, i.e.
+ * Python's math.fsum(x) / count, independent of summation order.  x: n
+ * doubles, host or device; mask: NULL (all selected) or n bytes (nonzero =
+ * selected), host or device; *mean_out (host) = 0.0 when nothing is selected;
+ * *count_out (host, may be NULL) = the number selected.  Exposed so the tests
+ * can pin the device reducer on adversarial arrays.  Errors: n < 0 or NULL
+ * x (n > 0) or NULL mean_out -> EINVAL; a selected value negative, inf or nan
+ * -> EINVAL (outside the contract; nothing written). */
+hm_status hm_exact_mean(hm_ctx *ctx, const double *x, int64_t n, const uint8_t *mask, double *mean_out,
+                        int32_t *count_out);
 
 /* ------------------------------------------------------------ utilities */
 

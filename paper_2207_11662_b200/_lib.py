@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhm.so")
 
 HM_OK, HM_EINVAL, HM_ERANGE, HM_ENOMEM, HM_ECUDA, HM_ESTATE = 0, -1, -2, -3, -4, -5
-HM_NAIVE, HM_CC1, HM_CC2, HM_CC2_AVG = 0, 1, 2, 3
+HM_NAIVE, HM_CC1, HM_CC2, HM_CC2_AVG, HM_CC1_RARY = 0, 1, 2, 3, 4
 STATUS_NAMES = {0: "HM_OK", -1: "HM_EINVAL", -2: "HM_ERANGE", -3: "HM_ENOMEM", -4: "HM_ECUDA",
                 -5: "HM_ESTATE"}
 
@@ -48,6 +48,7 @@ SIGNATURES = {
     "hm_compose": (ctypes.c_int32, [vp, ctypes.c_int32, c_i32p, ctypes.c_int32, ctypes.c_int32, vp, c_i32p]),
     "hm_set_metrics": (ctypes.c_int32, [vp, ctypes.c_int32, vp, ctypes.c_int64, vp, ctypes.c_int64,
                                         ctypes.POINTER(ctypes.c_double)]),
+    "hm_exact_mean": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, ctypes.POINTER(ctypes.c_double), c_i32p]),
     "hm_sync": (ctypes.c_int32, [vp]),
     "hm_debug_counts": (ctypes.c_int32, [vp, vp, ctypes.c_int32]),
     "hm_get_stats": (ctypes.c_int32, [vp, ctypes.POINTER(HmStats), ctypes.c_int]),

@@ -178,7 +178,7 @@ void closeness_combine(hm_ctx *ctx, Graph &G, const uint64_t *d_S_total);
 // exact (correctly rounded) sum of masked non-negative doubles, then mean = sum / count;
 // result written to device double *d_mean (count taken from mask popcount or n)
 void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask_or_null,
-                double *d_mean_out, int32_t *d_count_out);
+                double *d_mean_out, int32_t *d_count_out, int32_t *d_bad_out = nullptr);
 void degrees(hm_ctx *ctx, const Graph &G, int32_t *d_deg);
 // keys ordering closeness descending: ~bits(c) (c >= 0, so bit patterns are monotone)
 void closeness_desc_keys(hm_ctx *ctx, const double *d_c, int32_t V, uint64_t *d_keys);

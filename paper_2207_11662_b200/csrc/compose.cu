@@ -25,7 +25,8 @@ struct LayerPtrs {
 
 // CC2 (Alg. 1): estSumDist(u) = max_i sumDist_i(u) (n-penalty
 // sums, reading Z3).  Ranking by Eq. 1 (n-1)/est descending == est ascending.
-__global__ void k_cc2_keys(LayerPtrs L, int V, uint64_t *key) {
+__global__ void k_cc2_keys(LayerPtrs L, int V, uint64_t *key, int32_t *count, int K) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = K;      // CC2 ranks every vertex
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         uint64_t e = L.pen[0][v];
         for (int i = 1; i < L.r; ++i) e = max(e, L.pen[i][v]);
@@ -219,6 +220,13 @@ __global__ void k_set_metrics(const unsigned long long *cnt, double *out) {
     out[6] = nab;
 }
 
+// ids past the set size become -1 (device outputs of the sync-free path)
+__global__ void k_pad_ids(int32_t *ids, int K, const int32_t *count) {
+    const int n = *count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x)
+        if (i >= n) ids[i] = -1;
+}
+
 }  // namespace
 
 void set_metrics(hm_ctx *ctx, int32_t V, const int32_t *d_est, int64_t n_est, const int32_t *d_gt,
@@ -249,6 +257,10 @@ void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t
     cudaStream_t s = ctx->stream;
     const int r = (int)gs.size();
     HM_REQUIRE(r >= 2 && r <= RMAX, HM_EINVAL, "compose needs 2 <= r <= 8 layers");
+    // CC1 is defined for a pair of layers; the flat r-ary form (Z12) is opt-in
+    HM_REQUIRE(heuristic != HM_CC1 || r == 2, HM_EINVAL,
+               "CC1 is defined for two layers only (PAPER.md:477-507); use HM_CC1_RARY for the flat r-ary "
+               "reading Z12");
     const int V = gs[0]->V;
     HM_REQUIRE(K >= 1 && K <= V, HM_EINVAL, "K must be in [1, V]");
     LayerPtrs L;
@@ -263,61 +275,76 @@ void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t
         L.cl[i] = gs[i]->col.as<int32_t>();
     }
     const unsigned g = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
-    const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
-    Buf keys((size_t)V * 8, s), ids((size_t)K * 4, s), cnt(8, s);
-    HM_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
-    int32_t Kout = K;
+    // ids[0..K) ranked ids, ids[K] = |result set| (one D2H for host outputs)
+    Buf keys((size_t)V * 8, s), ids((size_t)(K + 1) * 4, s);
+    int32_t *d_ids = ids.as<int32_t>();
+    int32_t *d_cnt = d_ids + K;
+    HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
     if (heuristic == HM_CC2) {
-        k_cc2_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>());
+        k_cc2_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>(), d_cnt, K);
         check_launch("k_cc2_keys");
         count_launch(ctx);
-        topk(ctx, keys.as<uint64_t>(), V, K, ids.as<int32_t>());
-        if (count_out) *count_out = K;
-    } else if (heuristic == HM_NAIVE || heuristic == HM_CC1 || heuristic == HM_CC2_AVG) {
-        if (heuristic == HM_NAIVE) {
-            k_naive_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>(), cnt.as<int32_t>());
-            check_launch("k_naive_keys");
-            count_launch(ctx);
-        } else if (heuristic == HM_CC2_AVG) {
-            Buf score((size_t)V * 8, s), mu(16, s);
-            k_cc2_scores<<<g, TB, 0, s>>>(L, V, score.as<double>());
-            exact_mean(ctx, score.as<double>(), V, nullptr, mu.as<double>(), nullptr);
-            k_above_keys<<<g, TB, 0, s>>>(score.as<double>(), mu.as<double>(), V, keys.as<uint64_t>(),
-                                         cnt.as<int32_t>());
-            check_launch("cc2 above-average");
-            count_launch(ctx, 2);
-        } else {
-            Buf mindeg((size_t)V * 4, s), ratio((size_t)V * r * 8, s), fin((size_t)V, s);
-            Buf avgs((size_t)(r + 1) * 8, s), R((size_t)((V + 31) / 32) * 4, s);
-            HM_CUDA(cudaMemsetAsync(R.p, 0, R.bytes, s));
-            k_cc1_ratios<<<g, TB, 0, s>>>(L, V, mindeg.as<int32_t>(), ratio.as<double>(), fin.as<uint8_t>());
-            count_launch(ctx);
-            for (int i = 0; i < r; ++i)
-                exact_mean(ctx, ratio.as<double>() + (size_t)i * V, V, fin.as<uint8_t>(), avgs.as<double>() + i,
-                           nullptr);
-            k_cc1_avgand<<<1, 32, 0, s>>>(avgs.as<double>(), r, avgs.as<double>() + r);
-            Buf icnt((size_t)V * 4, s);
-            HM_CUDA(cudaMemsetAsync(icnt.p, 0, icnt.bytes, s));
-            const int64_t nnz0 = gs[0]->nnz;
-            const unsigned ga = grid_for(nnz0 > V ? nnz0 : (int64_t)V, TB, (int64_t)ctx->num_sms * 16);
-            for (int pass = 0; pass < 2; ++pass)
-                k_cc1_main<<<ga, TB, 0, s>>>(L, V, nnz0, ratio.as<double>(), avgs.as<double>() + r,
-                                             icnt.as<int32_t>(), R.as<uint32_t>(), pass);
-            k_cc1_keys<<<g, TB, 0, s>>>(L, V, R.as<uint32_t>(), mindeg.as<int32_t>(), keys.as<uint64_t>(),
-                                       cnt.as<int32_t>());
-            check_launch("cc1");
-            count_launch(ctx, 4);
-        }
-        int32_t nR = 0;
-        HM_CUDA(cudaMemcpyAsync(&nR, cnt.p, 4, cudaMemcpyDeviceToHost, s));
-        HM_CUDA(cudaStreamSynchronize(s));
-        Kout = nR < K ? nR : K;
-        if (Kout > 0) topk(ctx, keys.as<uint64_t>(), V, Kout, ids.as<int32_t>());
-        if (count_out) *count_out = nR;
+    } else if (heuristic == HM_NAIVE) {
+        k_naive_keys<<<g, TB, 0, s>>>(L, V, keys.as<uint64_t>(), d_cnt);
+        check_launch("k_naive_keys");
+        count_launch(ctx);
+    } else if (heuristic == HM_CC2_AVG) {
+        Buf score((size_t)V * 8, s), mu(16, s);
+        k_cc2_scores<<<g, TB, 0, s>>>(L, V, score.as<double>());
+        exact_mean(ctx, score.as<double>(), V, nullptr, mu.as<double>(), nullptr);
+        k_above_keys<<<g, TB, 0, s>>>(score.as<double>(), mu.as<double>(), V, keys.as<uint64_t>(), d_cnt);
+        check_launch("cc2 above-average");
+        count_launch(ctx, 2);
+    } else if (heuristic == HM_CC1 || heuristic == HM_CC1_RARY) {
+        Buf mindeg((size_t)V * 4, s), ratio((size_t)V * r * 8, s), fin((size_t)V, s);
+        Buf avgs((size_t)(r + 1) * 8, s), R((size_t)((V + 31) / 32) * 4, s);
+        HM_CUDA(cudaMemsetAsync(R.p, 0, R.bytes, s));
+        k_cc1_ratios<<<g, TB, 0, s>>>(L, V, mindeg.as<int32_t>(), ratio.as<double>(), fin.as<uint8_t>());
+        count_launch(ctx);
+        for (int i = 0; i < r; ++i)
+            exact_mean(ctx, ratio.as<double>() + (size_t)i * V, V, fin.as<uint8_t>(), avgs.as<double>() + i,
+                       nullptr);
+        k_cc1_avgand<<<1, 32, 0, s>>>(avgs.as<double>(), r, avgs.as<double>() + r);
+        Buf icnt((size_t)V * 4, s);
+        HM_CUDA(cudaMemsetAsync(icnt.p, 0, icnt.bytes, s));
+        const int64_t nnz0 = gs[0]->nnz;
+        const unsigned ga = grid_for(nnz0 > V ? nnz0 : (int64_t)V, TB, (int64_t)ctx->num_sms * 16);
+        for (int pass = 0; pass < 2; ++pass)
+            k_cc1_main<<<ga, TB, 0, s>>>(L, V, nnz0, ratio.as<double>(), avgs.as<double>() + r,
+                                         icnt.as<int32_t>(), R.as<uint32_t>(), pass);
+        k_cc1_keys<<<g, TB, 0, s>>>(L, V, R.as<uint32_t>(), mindeg.as<int32_t>(), keys.as<uint64_t>(), d_cnt);
+        check_launch("cc1");
+        count_launch(ctx, 4);
     } else {
         throw Error(HM_EINVAL, "unknown heuristic");
     }
-    if (Kout > 0) copy_out(ctx, ids_out, ids.p, (size_t)Kout * 4);
+    // Top-K over all V keys: members' keys are below ~0 (non-members), so the first
+    // min(K, |R|) ranked ids are the members and no host round trip is needed before it.
+    topk(ctx, keys.as<uint64_t>(), V, K, d_ids);
+    const bool dev_ids = is_device_ptr(ids_out);
+    const bool dev_cnt = count_out == nullptr || is_device_ptr(count_out);
+    if (dev_ids && dev_cnt) {                         // fully stream-ordered: no synchronisation
+        k_pad_ids<<<grid_for(K, TB, (int64_t)ctx->num_sms * 4), TB, 0, s>>>(d_ids, K, d_cnt);
+        check_launch("k_pad_ids");
+        count_launch(ctx);
+        HM_CUDA(cudaMemcpyAsync(ids_out, d_ids, (size_t)K * 4, cudaMemcpyDeviceToDevice, s));
+        if (count_out) HM_CUDA(cudaMemcpyAsync(count_out, d_cnt, 4, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    std::vector<int32_t> h((size_t)K + 1);
+    HM_CUDA(cudaMemcpyAsync(h.data(), d_ids, (size_t)(K + 1) * 4, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    const int32_t nR = h[K];
+    const int32_t Kout = nR < K ? nR : K;
+    if (dev_ids) {
+        if (Kout > 0) HM_CUDA(cudaMemcpyAsync(ids_out, d_ids, (size_t)Kout * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
+        for (int i = 0; i < Kout; ++i) ids_out[i] = h[i];
+    }
+    if (count_out) {
+        if (dev_cnt) HM_CUDA(cudaMemcpyAsync(count_out, d_cnt, 4, cudaMemcpyDeviceToDevice, s));
+        else *count_out = nR;
+    }
 }
 
 }  // namespace hm

@@ -76,8 +76,9 @@ __global__ void __launch_bounds__(BLOCK) k_exact_accum(const double *__restrict_
 
 // One thread: carry-normalise, round to nearest even, divide by count.
 __global__ void k_exact_finish(const unsigned long long *acc_in, const unsigned long long *count,
-                               double *mean_out, int32_t *count_out) {
+                               double *mean_out, int32_t *count_out, const int32_t *bad, int32_t *bad_out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (bad_out) *bad_out = *bad;
     uint32_t L[NLIMB + 2];
     unsigned long long carry = 0;
     for (int i = 0; i < NLIMB; ++i) {
@@ -116,7 +117,7 @@ __global__ void k_exact_finish(const unsigned long long *acc_in, const unsigned 
 }  // namespace
 
 void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask_or_null,
-                double *d_mean_out, int32_t *d_count_out) {
+                double *d_mean_out, int32_t *d_count_out, int32_t *d_bad_out) {
     cudaStream_t s = ctx->stream;
     Buf acc((NLIMB + 2) * sizeof(unsigned long long), s);
     HM_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes, s));
@@ -129,7 +130,7 @@ void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask
         check_launch("k_exact_accum");
         count_launch(ctx);
     }
-    k_exact_finish<<<1, 32, 0, s>>>(d_acc, d_cnt, d_mean_out, d_count_out);
+    k_exact_finish<<<1, 32, 0, s>>>(d_acc, d_cnt, d_mean_out, d_count_out, d_bad, d_bad_out);
     check_launch("k_exact_finish");
     count_launch(ctx);
 }

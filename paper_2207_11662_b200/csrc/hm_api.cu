@@ -363,7 +363,7 @@ hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, i
     HM_API_BEGIN(ctx)
     HM_REQUIRE(layer_ids && ids_out, HM_EINVAL, "null argument");
     HM_REQUIRE(heuristic == HM_NAIVE || heuristic == HM_CC1 || heuristic == HM_CC2 ||
-                   heuristic == HM_CC2_AVG,
+                   heuristic == HM_CC2_AVG || heuristic == HM_CC1_RARY,
                HM_EINVAL, "unknown heuristic");
     HM_REQUIRE(r >= 2 && r <= 8, HM_EINVAL, "compose needs 2 <= r <= 8");
     std::set<int32_t> seen(layer_ids, layer_ids + r);
@@ -401,6 +401,34 @@ hm_status hm_set_metrics(hm_ctx *ctx, int32_t V, const int32_t *est_ids, int64_t
     memcpy(&bad, &h[7], 4);
     HM_REQUIRE(!bad, HM_ERANGE, "vertex id outside [0, V)");
     memcpy(out, h, 7 * sizeof(double));
+    HM_API_END(ctx)
+}
+
+hm_status hm_exact_mean(hm_ctx *ctx, const double *x, int64_t n, const uint8_t *mask, double *mean_out,
+                        int32_t *count_out) {
+    HM_API_BEGIN(ctx)
+    HM_REQUIRE(n >= 0 && mean_out && (n == 0 || x), HM_EINVAL, "bad argument");
+    cudaStream_t s = ctx->stream;
+    Buf stage((size_t)n * 9 + 16, s), res(32, s);
+    const double *dx = x;
+    const uint8_t *dm = mask;
+    if (n && !is_device_ptr(x)) {
+        HM_CUDA(cudaMemcpyAsync(stage.p, x, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        dx = stage.as<double>();
+    }
+    if (n && mask && !is_device_ptr(mask)) {
+        HM_CUDA(cudaMemcpyAsync(stage.as<char>() + (size_t)n * 8, mask, (size_t)n, cudaMemcpyHostToDevice, s));
+        dm = reinterpret_cast<const uint8_t *>(stage.as<char>() + (size_t)n * 8);
+    }
+    HM_CUDA(cudaMemsetAsync(res.p, 0, res.bytes, s));
+    int32_t *d_cnt_bad = reinterpret_cast<int32_t *>(res.as<double>() + 1);
+    exact_mean(ctx, dx, n, dm, res.as<double>(), d_cnt_bad, d_cnt_bad + 1);
+    struct { double mu; int32_t cnt, bad; } h;
+    HM_CUDA(cudaMemcpyAsync(&h, res.p, 16, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    HM_REQUIRE(!h.bad, HM_EINVAL, "a selected value is negative, inf or nan");
+    *mean_out = h.mu;
+    if (count_out) *count_out = h.cnt;
     HM_API_END(ctx)
 }
 

@@ -13,9 +13,10 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import HM_CC1, HM_CC2, HM_CC2_AVG, HM_NAIVE  # noqa: F401
+from ._lib import c_i32p
+from ._lib import HM_CC1, HM_CC1_RARY, HM_CC2, HM_CC2_AVG, HM_NAIVE  # noqa: F401
 
-HEURISTICS = {"naive": HM_NAIVE, "cc1": HM_CC1, "cc2": HM_CC2, "cc2_avg": HM_CC2_AVG}
+HEURISTICS = {"naive": HM_NAIVE, "cc1": HM_CC1, "cc2": HM_CC2, "cc2_avg": HM_CC2_AVG, "cc1_rary": HM_CC1_RARY}
 
 
 class HmError(RuntimeError):
@@ -233,17 +234,38 @@ class Context:
         return ids
 
     # -------------------------------------------------------- composition
-    def compose(self, heuristic, ids, K, out=None):
-        """heuristic in {'cc1','cc2','cc2_avg','naive'}.  Returns (ranked ids, |result set|)."""
+    def compose(self, heuristic, ids, K, out=None, count_out=None):
+        """heuristic in {'cc1','cc1_rary','cc2','cc2_avg','naive'}.  Returns (ranked ids, |result set|).
+        With ``out`` (a device tensor of K int32) and ``count_out`` (a device tensor of 1 int32)
+        the call is stream-ordered with no host synchronisation: ``out`` holds K entries,
+        -1 past |R|, and (out, count_out) is returned."""
         h = HEURISTICS[heuristic] if isinstance(heuristic, str) else int(heuristic)
         arr = (ctypes.c_int32 * len(ids))(*ids)
         buf = np.zeros(K, np.int32) if out is None else out
+        if count_out is not None:
+            self._check(self.L.hm_compose(self.h, h, arr, len(ids), int(K), _ptr(buf),
+                                          ctypes.cast(_ptr(count_out), c_i32p)))
+            return buf, count_out
         cnt = ctypes.c_int32()
         self._check(self.L.hm_compose(self.h, h, arr, len(ids), int(K), _ptr(buf), ctypes.byref(cnt)))
         n = cnt.value
         if out is None:
             return buf[:min(K, n)], n
         return buf, n
+
+    def exact_mean(self, x, mask=None):
+        """hm_exact_mean: (RN(exact sum of the selected x) / count, count).  x: float64 numpy
+        array or CUDA tensor; mask: None or uint8 of the same length."""
+        if isinstance(x, np.ndarray):
+            x = np.ascontiguousarray(x, dtype=np.float64)
+        if isinstance(mask, np.ndarray):
+            mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        n = int(x.shape[0])
+        mu = ctypes.c_double()
+        cnt = ctypes.c_int32()
+        self._check(self.L.hm_exact_mean(self.h, _ptr(x) if n else None, n, _ptr(mask) if n else None,
+                                         ctypes.byref(mu), ctypes.byref(cnt)))
+        return mu.value, cnt.value
 
     # ------------------------------------------------------------ metrics
     def set_metrics(self, V, est, gt):

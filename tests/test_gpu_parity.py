@@ -26,6 +26,11 @@ def hm():
     return Context
 
 
+def cc1_name(T):
+    """CC1 is the paper's two-layer heuristic; r > 2 uses the opt-in flat r-ary form (Z12)."""
+    return "cc1" if len(T) == 2 else "cc1_rary"
+
+
 def edges_arr(E):
     return np.array(sorted(E), dtype=np.int32).reshape(-1, 2)
 
@@ -222,7 +227,7 @@ def run_pipeline_and_compare(ctx, h, check_layers=True):
         rs = [refs[i] for i in T]
         ids2, n2 = ctx.compose("cc2", list(T), K)
         assert ids2.tolist() == O.cc2(rs, K)[0] and n2 == K
-        ids1, n1 = ctx.compose("cc1", list(T), K)
+        ids1, n1 = ctx.compose(cc1_name(T), list(T), K)
         r1, nr1, _ = O.cc1(rs, K)
         assert n1 == nr1 and ids1.tolist() == r1
         idsn, nn = ctx.compose("naive", list(T), K)
@@ -269,6 +274,130 @@ def test_cc1_golden_on_gpu(hm):
         a = ctx.and_aggregate([0, 1])
         assert ctx.closeness(a)["S"].tolist() == g["AND_S"]
         assert ctx.topk_closeness(a, 3).tolist() == g["GT_top3"]
+
+
+def test_cc1_golden_eight_vertex_on_gpu(hm):
+    """the second hand-executed instance (isolated vertices, avgAND tie, |I| = 1)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cc1_eight_vertex.json")))
+    V = g["V"]
+    with hm() as ctx:
+        ctx.load_layers(V, [np.array(g["L1"], np.int32), np.array(g["L2"], np.int32)])
+        for i, t in ((0, "1"), (1, "2")):
+            got = ctx.closeness(i)
+            assert got["S"].tolist() == g["S" + t] and got["pen"].tolist() == g["pen" + t]
+            assert ctx.cc_nodes(i)[0].tolist() == g["CH" + t]
+        ids, n = ctx.compose("cc1", [0, 1], V)
+        assert ids.tolist() == g["CC1_ranked"] and n == len(g["CC1_R"])
+        assert ctx.compose("cc1_rary", [1, 0], V)[0].tolist() == g["CC1_ranked"]
+        assert ctx.compose("cc2", [0, 1], 4)[0].tolist() == g["CC2_top4"]
+        assert ctx.compose("cc2_avg", [0, 1], V)[0].tolist() == g["CC2_avg"]
+        assert ctx.compose("naive", [0, 1], V)[0].tolist() == g["naive"]
+        a = ctx.and_aggregate([0, 1])
+        ra = ctx.closeness(a)
+        assert ra["S"].tolist() == g["AND_S"] and ra["pen"].tolist() == g["AND_pen"]
+        assert ctx.cc_nodes(a)[0].tolist() == g["GT_CH"]
+        assert ctx.topk_closeness(a, 3).tolist() == g["GT_top3"]
+
+
+def test_cc1_pair_only_and_rary_opt_in(hm):
+    """HM_CC1 is the paper's pair heuristic (PAPER.md:477-507): r > 2 is rejected;
+    HM_CC1_RARY is the explicit flat r-ary reading (Z12) and equals HM_CC1 at r = 2."""
+    from paper_2207_11662_b200 import HmError
+    h = build_config("C2", V=1024)
+    with hm() as ctx:
+        ctx.load_layers(h.V, h.layers)
+        for i in range(3):
+            ctx.closeness(i)
+        with pytest.raises(HmError, match="HM_EINVAL"):
+            ctx.compose("cc1", [0, 1, 2], 10)
+        for T in ([0, 1], [1, 2], [2, 0]):
+            assert ctx.compose("cc1", T, 50)[0].tolist() == ctx.compose("cc1_rary", T, 50)[0].tolist()
+        Es = [set(map(tuple, L.tolist())) for L in h.layers]
+        rs = [O.analyze(h.V, E) for E in Es]
+        r1, n1, _ = O.cc1(rs, 50)
+        ids, n = ctx.compose("cc1_rary", [0, 1, 2], 50)
+        assert ids.tolist() == r1 and n == n1
+
+
+def test_compose_device_outputs_sync_free(hm):
+    """device ids + device count: K entries, -1 past |R|, same ranking as the host path."""
+    import torch
+    h = build_config("C5", V=4096)
+    with hm() as ctx:
+        ctx.load_layers(h.V, h.layers)
+        for i in range(3):
+            ctx.closeness(i)
+        T = [0, 1, 2]
+        for heur in ("cc1_rary", "cc2", "naive", "cc2_avg"):
+            for K in (1, 7, 500, h.V):
+                ref, n = ctx.compose(heur, T, K)
+                out = torch.full((K,), -7, dtype=torch.int32, device="cuda")
+                cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+                ctx.compose(heur, T, K, out=out, count_out=cnt)
+                torch.cuda.synchronize()
+                got = out.cpu().numpy()
+                assert int(cnt.item()) == n
+                m = min(K, n)
+                assert got[:m].tolist() == ref.tolist()
+                assert (got[m:] == -1).all()
+
+
+def test_exact_mean_adversarial_on_gpu(hm):
+    """GPU pin of the exact-sum reducer (the mean behind "higher than the
+    average", and Eq. 3's averages): hm_exact_mean must equal
+    math.fsum(x) / n (correctly rounded sum, one IEEE division), checked with Fraction, on arrays
+    where plain summation is wrong: long tails of tiny terms, spans from 2^-1074 to 2^37,
+    round-half-even ties, and sticky bits below the top three 32-bit limbs."""
+    import math
+    from fractions import Fraction
+    import torch
+    from paper_2207_11662_b200 import HmError
+
+    def want(xs):
+        exact = sum((Fraction(x) for x in xs), Fraction(0))
+        s = float(exact)                                  # Fraction -> float rounds half to even
+        assert s == math.fsum(xs)
+        return s / len(xs) if xs else 0.0
+
+    rng = random.Random(6)
+    tiny = 5e-324                                          # 2^-1074
+    cases = [
+        [1.0] + [2.0 ** -53] * 1000,                       # tail that left-to-right drops
+        [1.0, 2.0 ** -53],                                 # exact tie -> even (1.0)
+        [1.0 + 2.0 ** -52, 2.0 ** -53],                    # tie -> even (rounds up)
+        [1.0, 2.0 ** -53, 2.0 ** -140],                    # tie broken by a sticky bit far below
+        [1.0, 2.0 ** -53, tiny],                           # ... by a subnormal
+        [2.0 ** 37, 2.0 ** -16, 2.0 ** -70, tiny],         # 2^37 .. 2^-1074
+        [2.0 ** 37] * 999 + [2.0 ** -1000] * 3,
+        [1.0 / 3.0] * 999 + [2.0 ** -106],
+        [0.1] * 10,
+        [tiny] * 12345,                                    # subnormals only
+        [2.0 ** -1022 - tiny, tiny],                       # subnormal carry into the normal range
+        [float(2 ** 53 - 1), 0.5],                         # 2^53 - 1/2: tie at the top -> even
+        [float(2 ** 53 - 1), 0.5, 2.0 ** -200],
+        [rng.random() * 2.0 ** -rng.randint(0, 1074) for _ in range(20000)],
+        [rng.random() * 2.0 ** rng.randint(-60, 37) for _ in range(100000)],
+        [rng.randint(1, 10 ** 6) / rng.randint(10 ** 6, 10 ** 12) for _ in range(262144)],
+        [0.0] * 5,
+    ]
+    with hm() as ctx:
+        for xs in cases:
+            mu, n = ctx.exact_mean(np.array(xs, dtype=np.float64))
+            assert n == len(xs)
+            assert mu == want(xs), (xs[:4], mu, want(xs))
+        # masked mean over the selected values only (Eq. 3's finite ratios, Z8), device input
+        x = np.array([rng.random() * 2.0 ** rng.randint(-30, 30) for _ in range(5000)])
+        m = (np.arange(5000) % 3 != 0).astype(np.uint8)
+        sel = [float(v) for v, k in zip(x, m) if k]
+        mu, n = ctx.exact_mean(torch.from_numpy(x).cuda(), torch.from_numpy(m).cuda())
+        assert n == len(sel) and mu == want(sel)
+        assert ctx.exact_mean(np.zeros(0)) == (0.0, 0)
+        assert ctx.exact_mean(x, np.zeros(5000, np.uint8)) == (0.0, 0)
+        for bad in (-1.0, math.inf, math.nan):
+            with pytest.raises(HmError, match="HM_EINVAL"):
+                ctx.exact_mean(np.array([1.0, bad]))
 
 
 def test_set_metrics_edge_cases(hm):
@@ -360,7 +489,7 @@ def test_sharded_closeness(hm, name, V):
             full[g] = ctx.closeness(g)
             full[g]["topk"] = ctx.topk_closeness(g, h.K).tolist()
         ref_cc2 = ctx.compose("cc2", T, h.K)[0].tolist()
-        ref_cc1 = ctx.compose("cc1", T, h.K)
+        ref_cc1 = ctx.compose(cc1_name(T), T, h.K)
         whole = {g: ctx.closeness_partial(g, 0, 1) for g in gids}
         for nshards in (1, 2, 3):
             for g in gids:
@@ -376,7 +505,7 @@ def test_sharded_closeness(hm, name, V):
                 assert np.array_equal(got["c"].view(np.uint64), full[g]["c"].view(np.uint64))
                 assert ctx.topk_closeness(g, h.K).tolist() == full[g]["topk"]
             assert ctx.compose("cc2", T, h.K)[0].tolist() == ref_cc2
-            ids, n = ctx.compose("cc1", T, h.K)
+            ids, n = ctx.compose(cc1_name(T), T, h.K)
             assert n == ref_cc1[1] and ids.tolist() == ref_cc1[0].tolist()
         with pytest.raises(Exception):
             ctx.closeness_partial(gids[0], 2, 2)

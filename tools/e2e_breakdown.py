@@ -23,7 +23,7 @@ with Context(0) as ctx:
         for T, g in zip(h.subsets, ands):
             ctx.topk_closeness(g, h.K); mark("topk")
             ctx.compose("cc2", list(T), h.K); mark("cc2")
-            ctx.compose("cc1", list(T), h.K); mark("cc1")
+            ctx.compose("cc1" if len(T) == 2 else "cc1_rary", list(T), h.K); mark("cc1")
             ctx.compose("naive", list(T), h.K); mark("naive")
             ctx.free_graph(g); mark("free")
         print(" ".join(f"{n}={1e3 * (t - marks[i][1]):.1f}" for i, (n, t) in enumerate(marks[1:])),
