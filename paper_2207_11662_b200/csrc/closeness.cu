@@ -553,9 +553,9 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // graphs (many isolated vertices) need far less than V rows of state
     int64_t frows = V;
     int32_t h_heavy = 0;
-    // small graphs (<= 256 MB of frontier rows at V rows) skip the row count and its host round trip:
+    // small graphs (<= 256 MB of visited-set rows at V rows) skip the row count and its host round trip:
     // F is sized for V rows and the heavy-row arrays for the bound nnz / (heavy_deg + 1)
-    const bool count_rows = (int64_t)V * (int64_t)rowb * 3 > ((int64_t)256 << 20);
+    const bool count_rows = (int64_t)V * (int64_t)rowb * 2 > ((int64_t)256 << 20);
     if (!count_rows) {
         if (frows < 32) frows = 32;                                  // as the counted path
         const int64_t bound = U.nnz / ((int64_t)heavy_deg + 1);
@@ -575,8 +575,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         if (frows < 32) frows = 32;
     }
     const size_t bmw = (((size_t)(V + 31) / 32) + 4) & ~(size_t)3;   // multiple of 4 words (16-B rows for uint4 copies)
-    Buf F0((size_t)frows * rowb, s), F1((size_t)frows * rowb, s), F2((size_t)frows * rowb, s);
-    Buf bms(bmw * 5 * 4, s), Srel((size_t)V * 8, s), Kb((size_t)V * 2 + 16, s), flags(128, s);
+    Buf F0((size_t)frows * rowb, s), F1((size_t)frows * rowb, s);
+    Buf bms(bmw * 6 * 4, s), Srel((size_t)V * 8, s), Kb((size_t)V * 2 + 16, s), flags(128, s);
     HM_CUDA(cudaMemsetAsync(Srel.p, 0, Srel.bytes, s));
     HM_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, s));
     BfsArgs a;
@@ -617,10 +617,11 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     }
     a.F[0] = F0.as<uint64_t>();
     a.F[1] = F1.as<uint64_t>();
-    a.F[2] = F2.as<uint64_t>();
     uint32_t *bm = bms.as<uint32_t>();
-    for (int i = 0; i < 4; ++i) a.chg[i] = bm + i * bmw;
-    a.done = bm + 4 * bmw;
+    for (int i = 0; i < 3; ++i) a.chg[i] = bm + i * bmw;
+    a.done = bm + 3 * bmw;
+    a.has = bm + 4 * bmw;
+    a.par = bm + 5 * bmw;
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
     a.hints = ctx->params.bfs_hints;
@@ -656,7 +657,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         while ((32 >> us) > unit && us < 4) ++us;     // 32 >> us rows per unit
         a.unit_shift = us;
     }
-    a.chg_smem = (ctx->params.bfs_chg_smem && bmw * 4 * 2 <= 80 * 1024) ? 1 : 0;
+    a.chg_smem = (ctx->params.bfs_chg_smem && bmw * 4 <= 80 * 1024) ? 1 : 0;
     a.S = Srel.as<uint64_t>();
     a.flags = flags.as<int32_t>();
     // fused level barrier: two zeroed counters in the same (zeroed) 128-B flags block

@@ -10,13 +10,20 @@
 // d(s,v) = d(v,s), summing d * popc(new bits of row v at level d) over all
 // batches gives S(v) directly -- no transpose, one owner per row.
 //
-// No visited array.  On an undirected graph a source s in
-//   acc_d(v) = OR over neighbours u of F_{d-1}(u)
-// has d(s,u) = d-1 for some neighbour u, hence d(s,v) in {d-2, d-1, d}; so
-//   new_d(v) = acc_d(v) & ~F_{d-1}(v) & ~F_{d-2}(v)
-// is exactly the set of sources at distance d.  A row therefore reads only
-// its own two previous frontier rows and writes one frontier row per change.
-// Completion (every window source reached) comes from a 16-bit per-row count K.
+// Visited sets, double-buffered, no frontier array.  V_d(v) = sources within
+// distance d of v.  On an undirected graph
+//   V_d(v) = V_{d-1}(v) | OR over neighbours u of V_{d-1}(u),
+// and only neighbours that CHANGED at level d-1 can contribute a new source (a
+// source s in V_{d-2}(u) has d(s,v) <= d-1, already in V_{d-1}(v)).  So
+//   new_d(v) = (OR over u in N(v) changed at d-1 of V_{d-1}(u)) & ~V_{d-1}(v)
+// is exactly the set of sources at distance d.  A row that changes at level d
+// writes V_d(v) into buffer F[d & 1]; a row changed at d-1 is therefore gathered
+// from F[(d-1) & 1], which nobody writes during level d, and a row reads its own
+// V_{d-1} from the buffer of the level that last wrote it (bitmaps has / par).
+// Per changed row and level: one own-row read and one row write (the frontier
+// recurrence F_d = acc & ~F_{d-1} & ~F_{d-2} of round 1 needed two reads and
+// three arrays).  Completion (every window source reached) comes from a 16-bit
+// per-row count K.
 //
 // Work reduction, all exact:
 //  * sources are batched per connected component (rows grouped by component,
@@ -46,7 +53,7 @@
 // barriers, half-CTA stream parts, a warp-wide pipelined item stream, per-CTA owned
 // rows, a level-1 push step -- are in git history up to commit 93c73e1.)
 //
-// Memory layout: frontier rows are W*8 bytes (512 B at the default W=64), row-major.
+// Memory layout: visited-set rows are W*8 bytes (512 B at the default W=64), row-major.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -225,8 +232,9 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
                                          uint32_t *done, uint16_t *K, uint64_t *S, int32_t *hclaim, ulonglong2 *s_red_,
                                  const unsigned long long *s_pl_, int s_nb, int n_items, int n_heavy,
                                  int hi, int n_giant, int64_t base, int d, const uint32_t *chp_s,
-                                 const uint32_t *chpp_s, const uint64_t *__restrict__ Fc,
-                                 const uint64_t *__restrict__ Fp, uint64_t *__restrict__ Fn, uint32_t *chn) {
+                                 uint32_t *has, uint32_t *par, const uint64_t *__restrict__ Fc,
+                                 const uint64_t *F0, const uint64_t *F1, uint64_t *__restrict__ Fn,
+                                 uint32_t *chn) {
     constexpr int T = W / 2;
     constexpr int TPB = BLOCK / T;
     constexpr int64_t B = 64 * W;
@@ -323,13 +331,9 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
             if (threadIdx.x == 0) hcnt[h] = 0;
         }
         if (tib == 0) {
+            // own visited set V_{d-1}(v): in the buffer of the level that last wrote it
             ulonglong2 vv = make_ulonglong2(0ull, 0ull);
-            if (bit_of(chp_s, v)) vv = ld2(Fc + (size_t)v * W + 2 * tl);
-            if (bit_of(chpp_s, v)) {
-                const ulonglong2 x = ld2(Fp + (size_t)v * W + 2 * tl);
-                vv.x |= x.x;
-                vv.y |= x.y;
-            }
+            if (bit_of(has, v)) vv = ld2((bit_of(par, v) ? F1 : F0) + (size_t)v * W + 2 * tl);
             const ulonglong2 nw = make_ulonglong2(acc.x & ~vv.x, acc.y & ~vv.y);
             int cnt = __popcll(nw.x) + __popcll(nw.y);
 #pragma unroll
@@ -344,7 +348,7 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
                 for (int o = T / 2; o > 0; o >>= 1) wsum += __shfl_xor_sync(tmask, wsum, o);
             }
             if (cnt) {
-                st2(Fn + (size_t)v * W + 2 * tl, nw);
+                st2(Fn + (size_t)v * W + 2 * tl, make_ulonglong2(nw.x | vv.x, nw.y | vv.y));   // V_d(v)
                 if (tl == 0) {
                     const int2 ci = (v < n_giant ? make_int2(0, n_giant) : cinfo[v]);
                     int64_t nb = (int64_t)ci.y - base;
@@ -358,6 +362,9 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
                         S[v] += (uint64_t)d * (uint64_t)cnt;
                     const uint32_t vbit = 1u << (v & 31);
                     atomicOr(&chn[v >> 5], vbit);
+                    atomicOr(&has[v >> 5], vbit);
+                    if (d & 1) atomicOr(&par[v >> 5], vbit);
+                    else atomicAnd(&par[v >> 5], ~vbit);
                     if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) atomicOr(&done[v >> 5], vbit);
                     any = true;
                 }
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 if (j >= 0 && j < nb) {
                     src = true;
                     dn = (nb == 1);
-                    uint64_t *f = a.F[0] + (size_t)v * W;
+                    uint64_t *f = a.F[0] + (size_t)v * W;           // V_0(v) = {v}
                     const int wj = (int)(j >> 6);
 #pragma unroll
                     for (int w = 0; w < W; w += 2)
@@ -457,7 +464,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             if (lane == 0) {
                 a.chg[0][g] = bs;     // changed at level 0: the sources
                 a.chg[1][g] = 0u;     // written at level 1
-                a.chg[3][g] = 0u;     // "level -1" (read as F_{d-2} at level 1)
+                a.has[g] = bs;        // only the sources hold a visited set, in buffer 0
+                a.par[g] = 0u;
                 a.done[g] = bd;
             }
         }
@@ -492,32 +500,27 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         if (a.dbgc && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
         for (;; ++d) {
             PROF_LEVEL(pf, d);
-            const uint64_t *__restrict__ Fc = a.F[(d + 2) % 3];    // F_{d-1}: gathered
-            const uint64_t *__restrict__ Fp = a.F[(d + 1) % 3];    // F_{d-2}: own rows only
-            uint64_t *__restrict__ Fn = a.F[d % 3];                // F_d: written
-            const uint32_t *chp = a.chg[(d + 3) & 3];
-            const uint32_t *chpp = a.chg[(d + 2) & 3];
-            uint32_t *chn = a.chg[d & 3];
-            uint32_t *chz = a.chg[(d + 1) & 3];
+            // rows changed at d-1 hold V_{d-1} in F[(d-1) & 1] (gathered); a row changing at d
+            // writes V_d into F[d & 1]; a row's own V_{d-1} is in the buffer of its last change
+            const uint64_t *__restrict__ Fc = a.F[(d - 1) & 1];
+            uint64_t *__restrict__ Fn = a.F[d & 1];
+            const uint64_t *F0 = a.F[0], *F1 = a.F[1];
+            const uint32_t *chp = a.chg[(d + 2) % 3];
+            uint32_t *chn = a.chg[d % 3];
+            uint32_t *chz = a.chg[(d + 1) % 3];
             for (int64_t w = gtid; w < ngroups; w += nthreads) chz[w] = 0u;
             if (gtid == 0) a.flags[(d + 1) % 3] = 0;
             if (HV && gtid == 0 && a.hclaim) a.hclaim[(d + 1) % 3] = 0;   // next level's claims
             // stage the two previous change bitmaps in shared memory
-            const uint32_t *chp_s = chp, *chpp_s = chpp;
+            const uint32_t *chp_s = chp;
             if (threadIdx.x == 0)
                 sm.next = a.interleave ? 0 : (int)(((int64_t)blockIdx.x * (ngroups << a.unit_shift)) / gridDim.x);
             if (a.chg_smem) {
                 const int nw4 = (int)((ngroups + 3) >> 2);
                 uint4 *d0 = s_dyn;
-                uint4 *d1 = s_dyn + (a.chg_words >> 2);
                 const uint4 *s0 = reinterpret_cast<const uint4 *>(chp);
-                const uint4 *s1 = reinterpret_cast<const uint4 *>(chpp);
-                for (int i = threadIdx.x; i < nw4; i += BLOCK) {
-                    d0[i] = s0[i];
-                    d1[i] = s1[i];
-                }
+                for (int i = threadIdx.x; i < nw4; i += BLOCK) d0[i] = s0[i];
                 chp_s = reinterpret_cast<const uint32_t *>(d0);
-                chpp_s = reinterpret_cast<const uint32_t *>(d1);
             }
             __syncthreads();
             PROF_MARK(pf, 0);
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             if (HV && !HM_HEAVY_DYN && n_items > 0)
                 any = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                 a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
-                                                hi, n_giant, base, d, chp_s, chpp_s, Fc, Fp, Fn, chn);
+                                                hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn);
             PROF_MARK(pf, 1);
 
             // ---- light rows: one warp per unit of 32 >> unit_shift rows of a 32-row group;
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 const unsigned amask = __ballot_sync(FULL, act);
                 PROF_MARK(pf, 2);
                 if (!amask) continue;                                    // warp-uniform
-                const uint32_t pword = chp_s[g], ppword = chpp_s[g];
+                const uint32_t hword = a.has[g], qword = a.par[g];     // own rows: state held, its buffer
                 uint32_t chg_bits = 0u, done_bits = 0u;
                 const int A0 = __shfl_sync(FULL, rp, q0);
                 const int A1 = __shfl_sync(FULL, rend, q0 + ur - 1);    // end of the unit's last row
@@ -639,12 +642,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         const int ke = has ? seg[sg + 1] : 0;
                         const int ri = has ? sr[kb] : 0;
                         const int v = (int)(g * 32 + ri);
-                        // row state, issued with the gathers: own F_{d-1}, F_{d-2}, K, S
-                        ulonglong2 vv[VEC], v2[VEC];
+                        // row state, issued with the gathers: own V_{d-1} (or the V_d an earlier
+                        // staging flush of this unit wrote), K, S
+                        ulonglong2 vv[VEC];
                         zero_row<VEC>(vv);
-                        zero_row<VEC>(v2);
-                        if (has && ((pword >> ri) & 1u)) ld_row<W, TL, VEC>(vv, Fc, v, ltl, pol_c);
-                        if (has && ((ppword >> ri) & 1u)) ld_row<W, TL, VEC>(v2, Fp, v, ltl, pol_p);
+                        if (has && ((chg_bits >> ri) & 1u)) {
+                            ld_row<W, TL, VEC>(vv, Fn, v, ltl);
+                        } else if (has && ((hword >> ri) & 1u)) {
+                            const bool q = (qword >> ri) & 1u;
+                            // written at d-1: also gathered by the neighbours this level
+                            ld_row<W, TL, VEC>(vv, q ? F1 : F0, v, ltl, q == (bool)((d - 1) & 1) ? pol_c : pol_p);
+                        }
                         int Kv = 0;
                         uint64_t Sv = 0;
                         if (has && ltl == 0) {
@@ -664,14 +672,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                             }
         #pragma unroll
                             for (int q = 0; q < GD; ++q) or_row<VEC>(acc, x[q]);
-                        }
-                        or_row<VEC>(vv, v2);
-                        // a row split over staging flushes already wrote part of F_d(v)
-                        ulonglong2 f0[VEC];
-                        zero_row<VEC>(f0);
-                        if (has && ((chg_bits >> ri) & 1u)) {
-                            ld_row<W, TL, VEC>(f0, Fn, v, ltl);
-                            or_row<VEC>(vv, f0);
                         }
                         int cnt = 0;
         #pragma unroll
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                             for (int o = TL / 2; o > 0; o >>= 1) wsum += __shfl_xor_sync(FULL, wsum, o);
                         }
                         if (cnt) {
-                            or_row<VEC>(acc, f0);
+                            or_row<VEC>(acc, vv);                         // V_d(v) = V_{d-1}(v) | new
                             st_row<W, TL, VEC>(Fn, v, ltl, acc, pol_n);
                             if (ltl == 0) {
                                 const int2 ci = comp_of(a, v, n_giant);
@@ -734,6 +734,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 if (lane == 0) {
                     if (chg_bits) {
                         atomicOr(&chn[g], chg_bits);
+                        atomicOr(&a.has[g], chg_bits);
+                        if (d & 1) atomicOr(&a.par[g], chg_bits);
+                        else atomicAnd(&a.par[g], ~chg_bits);
                         any = true;
                     }
                     if (done_bits) atomicOr(&a.done[g], done_bits);
@@ -753,7 +756,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             if (HV && HM_HEAVY_DYN && n_items > 0)
                 any |= heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                  a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
-                                                 n_heavy, hi, n_giant, base, d, chp_s, chpp_s, Fc, Fp, Fn, chn);
+                                                 n_heavy, hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn,
+                                                 chn);
             // one flag write per CTA (same-address stores from every group serialise in L2)
             const int any_cta = __syncthreads_or(any);
             if (any_cta && threadIdx.x == 0 && !a.lbar) a.flags[d % 3] = 1;
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             // dense-level model bytes of this batch: rows [0, hi) and their arcs
             const unsigned long long arcs = (unsigned long long)a.row_ptr[hi];
             a.counters[2] += (unsigned long long)d *
-                             (4ull * (hi + 1) + 4ull * arcs + 3ull * 8ull * W * (unsigned long long)hi);
+                             (4ull * (hi + 1) + 4ull * arcs + 2ull * 8ull * W * (unsigned long long)hi);
         }
     }
     PROF_FLUSH(pf, a.dbgc);
@@ -858,7 +862,7 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         default: return -1;
     }
 #undef HM_MSBFS_CASE
-    const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 * 2 : 0;
+    const size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 : 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) return -5;
     int maxb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, block, dyn) != cudaSuccess) return -2;

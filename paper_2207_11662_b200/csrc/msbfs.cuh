@@ -29,15 +29,18 @@ struct BfsArgs {
     int32_t *hcnt;               // [n_heavy] zeroed: items of the row done this level
     int32_t *hclaim;             // [3] heavy-item claim counters, rotated by level
     int32_t heavy_deg;
-    uint64_t *F[3];              // [n_live][W] frontier rows of levels d, d-1, d-2 (rotating)
-    uint32_t *chg[4];            // row bitmaps "changed at level", rotating over 4 levels
+    uint64_t *F[2];              // [n_live][W] visited-set rows V(v), double-buffered: a row that
+                                 // changes at level d writes V_d(v) into F[d & 1]
+    uint32_t *chg[3];            // row bitmaps "changed at level", rotating over 3 levels
     uint32_t *done;              // row bitmap: all sources of the row's window reached it
+    uint32_t *has;               // row bitmap: the row holds a visited set in this batch
+    uint32_t *par;               // row bitmap: parity of the level that last wrote the row (its buffer)
     uint16_t *K;                 // [n_live] window sources reached so far in this batch (self excluded)
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
-    int chg_smem;                // 1: stage the two previous change bitmaps in dynamic shared memory
+    int chg_smem;                // 1: stage the previous level's change bitmap in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
     int unit_shift;              // light-path work unit = 32 >> unit_shift rows of a 32-row group
     int shard, nshards;          // run batches i = shard, shard + nshards, ... only
@@ -46,7 +49,8 @@ struct BfsArgs {
     unsigned long long *planes;  // [BFS_T_BITS][W] scratch: T bit planes of the batch window
     int hints;                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
                                  // 4 F_d stores evict_last, 8 F_d stores evict_first, 16 evict_normal
-    unsigned long long *lbar;    // [2] fused level-barrier counters (zeroed); nullptr: grid.sync + flag
+    unsigned long long *lbar;    // [4] fused level-barrier counters (zeroed): arrivals and changed rows per
+                                 // level parity; nullptr: grid.sync + flag
     int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)
 };
 
