@@ -74,7 +74,7 @@ namespace {
 #define HM_BLOCK_PLAIN 448      // measured best for the plain kernel (2 CTAs x 14 warps, 73 registers)
 #endif
 #ifndef HM_BLOCK_WEIGHTED
-#define HM_BLOCK_WEIGHTED 384   // weighted (pruned) kernel: 85 registers, no spills
+#define HM_BLOCK_WEIGHTED 320   // weighted (pruned) kernel: measured best in round 2 (288: +28 %, 352: +4 %, 384: +3 %)
 #endif
 constexpr int BLOCK_PLAIN = HM_BLOCK_PLAIN, BLOCK_WEIGHTED = HM_BLOCK_WEIGHTED;
 #ifndef HM_CAP
@@ -832,7 +832,9 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     if (TL == 0) TL = (W == 64) ? 16 : W / 2;
     const int vec = W / (2 * TL);
     const int minb = blocks_per_sm == 1 ? 1 : 2;
-    if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : 2);
+    // gathers in flight per lane: 4 at W = 64 with 2 CTAs/SM (round 2, visited-set rows: C5 layer
+    // 68.8 -> 64.8 ms, AND 62.2 -> 58.6 ms against 2)
+    if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : (vec == 2 ? 4 : 2));
 #define HM_MSBFS_CASE(w, tl, gd, mb)                                                                     \
     case ((w * 100 + tl) * 100 + gd * 10 + mb):                                                          \
         kern = a.tw ? (const void *)msbfs_kernel<w, tl, gd, mb, true> : (const void *)msbfs_kernel<w, tl, gd, mb, false>; \
@@ -848,15 +850,17 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         HM_MSBFS_CASE(32, 16, 8, 1)
         HM_MSBFS_CASE(32, 8, 2, 2)
         HM_MSBFS_CASE(64, 32, 4, 2)
-    case ((64 * 100 + 16) * 100 + 2 * 10 + 2):                 // default: lean variants without heavy rows
+    case ((64 * 100 + 16) * 100 + 4 * 10 + 2):                 // default: lean variants without heavy rows
         if (a.hstart)
-            kern = a.tw ? (const void *)msbfs_kernel<64, 16, 2, 2, true> : (const void *)msbfs_kernel<64, 16, 2, 2, false>;
+            kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true> : (const void *)msbfs_kernel<64, 16, 4, 2, false>;
         else
-            kern = a.tw ? (const void *)msbfs_kernel<64, 16, 2, 2, true, false>
-                        : (const void *)msbfs_kernel<64, 16, 2, 2, false, false>;
+            kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false>
+                        : (const void *)msbfs_kernel<64, 16, 4, 2, false, false>;
         block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
         break;
+        HM_MSBFS_CASE(64, 16, 2, 2)
         HM_MSBFS_CASE(64, 16, 4, 1)
+        HM_MSBFS_CASE(64, 16, 8, 2)
         HM_MSBFS_CASE(64, 16, 8, 1)
         HM_MSBFS_CASE(64, 32, 8, 1)
         default: return -1;

@@ -561,8 +561,11 @@ def test_random_sweep_all_knobs(hm):
         for t in range(200):
             V, E = _shape(rng, t)
             res = O.analyze(V, E)
-            for k, vals in knobs.items():
-                ctx.set_param(k, rng.choice(vals))
+            pick = {k: rng.choice(vals) for k, vals in knobs.items()}
+            # gathers in flight: every instantiated value at W = 64, 2 CTAs/SM (the bench path)
+            pick["bfs_gd"] = rng.choice([0, 2, 4, 8]) if pick["bfs_words"] == 64 and pick["bfs_blocks_per_sm"] != 1 else 0
+            for k, v in pick.items():
+                ctx.set_param(k, v)
             ctx.load_layers(V, [edges_arr(E)])
             check_psi(V, E, ctx.closeness(0), res)
             if t % 6 == 0 and V >= 3:                 # sharded path, same knobs
