@@ -320,31 +320,78 @@ def run_ours(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                "steps_ms": [round(x, 3) for x in e_ms]}
 
-    # ---- roofline of the MS-BFS kernel
-    import json as _json
+    # ---- roofline of the MS-BFS kernel: per graph (one untimed pass, one MS-BFS launch per graph,
+    # library counters of that launch) and the headline over the dominant launches (the layers)
     peaks = {}
     try:
-        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    traffic, traffic_src = measured_traffic(args)
+    nbytes_row = 8 * args.words
+    per_graph = {}
+    if not args.shard and not args.fused:
+        ctx.sync()
+        ctx.stats(reset=True)
+        gl = [(f"L{i}", i) for i in range(len(h.layers))]
+        ands = []
+        for T in h.subsets:
+            g = ctx.and_aggregate(list(T))
+            ands.append(g)
+            gl.append(("AND" + "".join(map(str, T)), g))
+        for name, g in gl:
+            flush_l2()
+            ctx.closeness(g, out={})
+            ctx.sync()
+            sg = ctx.stats(reset=True)
+            t = sg["bfs_ms"] / 1e3
+            model = sg["bfs_model_bytes"]
+            comp = 2 * nbytes_row * sg["bfs_row_commits"] + sg["bfs_csr_bytes"]
+            e = {"ms": sg["bfs_ms"], "levels": sg["bfs_levels"], "batches": sg["bfs_batches"],
+                 "model_bytes": model, "compulsory_bytes": comp, "row_commits": sg["bfs_row_commits"],
+                 "model_frac": model / t / 1e9 / peak_gbs if t > 0 else None,
+                 "compulsory_frac": comp / t / 1e9 / peak_gbs if t > 0 else None}
+            nd = (traffic or {}).get("per_graph", {}).get(name)
+            if nd:
+                e["ncu_dram_bytes"] = nd["dram_bytes"]
+                e["ncu_ms"] = nd["duration_s"] * 1e3
+                e["ncu_dram_frac"] = nd["dram_bytes"] / nd["duration_s"] / 1e9 / peak_gbs
+                e["ncu_l2_hit_pct"] = nd.get("l2_hit_pct")
+            per_graph[name] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
+        for g in ands:
+            ctx.free_graph(g)
     n_bfs = max(1, st["bfs_launches"])
     bfs_ms_avg = st["bfs_ms"] / n_bfs
     levels_per_launch = st["bfs_levels"] / n_bfs
-    # SURVEY §8(d) dense-level model, accumulated by the kernel per batch over the rows and
-    # arcs that batch's BFS covers (the 2-core when pruning applies):
-    #   levels * (4 (rows + 1) row_ptr + 4 arcs col + 3 R rows state),  R = 8 W bytes per row
-    model_bytes = st["bfs_model_bytes"] / n_bfs
-    achieved = model_bytes / (bfs_ms_avg / 1e3) / 1e9 if bfs_ms_avg > 0 else 0.0
-    traffic, traffic_src = measured_traffic(args)
+    # headline: the dominant kernel, the plain MS-BFS launches of the layers (3 of the 4 launches of a
+    # C5 step, ~75 % of it); algorithmic bytes = SURVEY §8(d) dense-level model of this algorithm,
+    # accumulated by the kernel per batch:  L * (4 (rows + 1) + 4 arcs + 2 R rows),  R = 8 W bytes
+    layer_e = [v for k, v in per_graph.items() if k.startswith("L")]
+    if layer_e:
+        dom_ms = float(np.mean([v["ms"] for v in layer_e]))
+        dom_bytes = float(np.mean([v["model_bytes"] for v in layer_e]))
+        dom_traffic = (float(np.mean([v["ncu_dram_bytes"] for v in layer_e]))
+                       if all("ncu_dram_bytes" in v for v in layer_e) else None)
+        dom_name = "msbfs_kernel (plain instantiation), the layer launches"
+    else:                                   # --shard / --fused: all launches together
+        dom_ms = bfs_ms_avg
+        dom_bytes = st["bfs_model_bytes"] / n_bfs
+        dom_traffic = None
+        dom_name = "msbfs_kernel (all launches)"
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-            "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
-            "peak_source": peak_src,
-            "kernel": "msbfs_kernel",
-            "bytes_model": "SURVEY 8(d) dense-level, per batch: L*(4(rows+1)+4*arcs+3*R*rows), R=8W, summed by the kernel",
-            "bytes_per_launch": model_bytes, "ms_per_launch": bfs_ms_avg,
-            "levels_per_launch": levels_per_launch, "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9),
+            "frac": achieved / peak_gbs, "traffic": dom_traffic,
+            "traffic_source": traffic_src, "peak_source": peak_src, "kernel": dom_name,
+            "bytes_model": "SURVEY 8(d) dense-level model of the visited-set MS-BFS, per batch: "
+                           "L*(4(rows+1)+4*arcs+2*R*rows), R=8W bytes (own row read + row write), summed by the kernel",
+            "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
+            "per_graph": per_graph,
+            "per_graph_note": "model = dense-level bytes; compulsory = 2 R x rows actually changed + CSR per level; "
+                              "ncu_dram = dram__bytes_read+write of the same launch (ncu, serialised, cold cache)",
+            "levels_per_launch": levels_per_launch, "bfs_ms_per_launch_all": bfs_ms_avg,
+            "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9),
             "fused_graphs": 1 if (not args.fused) else len(arcs)}
     launches_per_step = st["launches"] / args.steps
 
@@ -407,30 +454,109 @@ def oracle_sample(V, E, seconds, threads, seed=0, graph=None):
     return u_total, t_total, s_total
 
 
+def src_digest():
+    """SHA-256 (16 hex) of the MS-BFS sources: a committed ncu traffic capture is used only for the
+    build it was taken on."""
+    import hashlib
+    m = hashlib.sha256()
+    for f in ("msbfs.cu", "msbfs.cuh", "closeness.cu", "prune.cu"):
+        m.update(open(os.path.join(ROOT, "paper_2207_11662_b200", "csrc", f), "rb").read())
+    return m.hexdigest()[:16]
+
+
 def measured_traffic(args):
-    """roofline.traffic: DRAM bytes per MS-BFS launch from the committed ncu capture
-    (tools/ncu_traffic.py) when it was taken on this config, batch width and L2 policy."""
+    """roofline traffic: DRAM bytes per MS-BFS launch from the committed ncu capture
+    (tools/ncu_traffic.py) when it was taken on this config, batch width, L2 policy and MS-BFS source."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_msbfs_traffic.json")))
+    sd = src_digest()
     for f in reversed(files):
         try:
             t = json.load(open(f))
         except Exception:
             continue
-        if t.get("config") == args.config and t.get("bfs_words") == args.words and t.get("bfs_hints") == args.hints:
-            return t["dram_bytes_per_launch"], os.path.relpath(f, ROOT)
+        if (t.get("config") == args.config and t.get("bfs_words") == args.words and t.get("bfs_hints") == args.hints
+                and t.get("src_sha") == sd):
+            return t, os.path.relpath(f, ROOT)
     return None, None
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_graphs(h):
+    """the oracle's graphs of one HoMLN step: the layers and the AND graph of every subset
+    (oracle and_aggregate, timed: part of the ground truth)."""
+    from oracle import oracle as O
+    graphs = [(f"L{i}", L) for i, L in enumerate(h.layers)]
+    Es = [set(map(tuple, L.tolist())) for L in h.layers]
+    t0 = time.perf_counter()
+    for T in h.subsets:
+        A = O.and_aggregate([Es[i] for i in T])
+        graphs.append(("AND" + "".join(map(str, T)), np.array(sorted(A), dtype=np.int32).reshape(-1, 2)))
+    return graphs, time.perf_counter() - t0
+
+
+def oracle_compose_seconds(h, V_small=2048):
+    """oracle composition time of one step (GT top-K, CC2, CC1, naive per subset; PAPER.md:205-211,
+    :436-507, :559-562), timed on the same recipe scaled to V_small (the oracle's plain Python then runs
+    in seconds) and scaled linearly to V (the paper: CC2 O(V), CC1 ~O(V) on average, PAPER.md:512-514,
+    :593).  Per-layer results are computed by the oracle (untimed)."""
+    from oracle import oracle as O
+    from synth import build_config as bc
+    name = h.name.split("@")[0]
+    hs = bc(name, V=min(h.V, V_small))
+    Es = [set(map(tuple, L.tolist())) for L in hs.layers]
+    res = [O.analyze(hs.V, E) for E in Es]
+    ra = {tuple(T): O.analyze(hs.V, O.and_aggregate([Es[i] for i in T])) for T in hs.subsets}
+    t0 = time.perf_counter()
+    for T in hs.subsets:
+        rs = [res[i] for i in T]
+        O.topk_closeness(ra[tuple(T)]["c"], hs.K)
+        O.cc2(rs, hs.K)
+        O.cc1(rs, hs.K)
+        O.naive(rs, hs.K)
+    return (time.perf_counter() - t0) * h.V / hs.V, hs.V
+
+
 def cpu_baseline(h, seconds):
+    """the oracle on this box's host cores (SURVEY 8(d) "Oracle timing"): a bounded source sample of
+    EVERY graph of the step (layers + AND graphs) with the plain C BFS, extrapolated to the whole
+    step by each graph's traversal units, plus the oracle's AND aggregation (full size, timed) and its
+    Python composition (scaled recipe, extrapolated)."""
     from oracle import _bfs
     threads = os.cpu_count() or 1
     used = _bfs.num_threads(threads)
-    E = h.layers[0]
-    u, t, n = oracle_sample(h.V, E, seconds, threads)
-    return {"value": u / t, "unit": "TEPS", "cores": used, "kind": "oracle",
-            "sample": f"oracle plain per-source BFS (C, OpenMP over sources, BFS loop timed) from {n} random "
-                      f"sources of {h.name} layer 0 ({t:.1f} s; TEPS = sum of m_c over sampled sources / time)"}
+    graphs, and_s = oracle_graphs(h)
+    per = max(1.0, seconds / len(graphs))
+    U, Tt, N, bfs_s, pg = 0, 0.0, 0, 0.0, {}
+    for name, E in graphs:
+        u, t, n = oracle_sample(h.V, E, per, threads)
+        W_g = int(_component_edges(h.V, E).sum())         # sum over sources of their component's edges
+        teps = u / t
+        bfs_s += W_g / teps
+        U, Tt, N = U + u, Tt + t, N + n
+        pg[name] = {"teps": teps, "sources": n, "seconds": round(t, 3), "units_W": W_g}
+    comp_s, v_small = oracle_compose_seconds(h)
+    return {"value": U / Tt, "unit": "TEPS", "cores": used, "kind": "oracle",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "s_per_homln_extrapolated": bfs_s + and_s + comp_s,
+            "breakdown_s": {"bfs_extrapolated": bfs_s, "and_aggregate": and_s,
+                            "compose_extrapolated": comp_s},
+            "per_graph": pg,
+            "sample": f"oracle plain per-source BFS (C, OpenMP over sources, BFS loop timed) from random source "
+                      f"samples of all {len(graphs)} graphs of {h.name} (~{per:.0f} s each, {N} sources); TEPS = "
+                      f"sampled units / time; s/HoMLN = sum over graphs of W / TEPS (extrapolated) + the oracle's "
+                      f"AND aggregation (timed, full size) + its Python composition (timed at V={v_small}, "
+                      f"scaled by V)"}
 
 
 def run_reference(args, rank, world):

@@ -259,14 +259,19 @@ typedef struct {
     int64_t bfs_levels;
     int64_t bfs_batches;
     double bfs_model_bytes;   /* SURVEY §8(d) dense-level bytes of the MS-BFS launches, summed per batch:
-                                 levels * (4 (rows + 1) + 4 arcs + 3 * 8 W * rows) over the batch's
-                                 BFS rows and arcs (the pruned core when 2-core pruning applies) */
+                                 levels * (4 (rows + 1) + 4 arcs + 2 * 8 W * rows) over the batch's
+                                 BFS rows and arcs (the pruned core when 2-core pruning applies); 2 state
+                                 rows per row and level: the own visited set read and the new one written */
+    int64_t bfs_row_commits;  /* rows changed, summed over levels and batches (each one own-row read and one
+                                 8 W-byte row write: the compulsory state traffic); needs bfs_fbar = 1 */
+    double bfs_csr_bytes;     /* CSR bytes of the same model: levels * (4 (rows + 1) + 4 arcs) per batch */
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
 
 /* Debug: copy the counters of the last MS-BFS launch made with
  * hm_set_param("bfs_dbg", 2): out[d] = source batches that ran level d,
- * out[4096+d] = nanoseconds spent in level d (summed over batches), and in
+ * out[4096+d] = nanoseconds spent in level d (summed over batches),
+ * out[12288+d] = rows changed at level d (summed over batches), and in
  * HM_MSBFS_PROF builds out[8192..8204] = per-phase warp cycles and counts.
  * n <= 335872 uint64 (host).  ESTATE if no such launch happened. */
 hm_status hm_debug_counts(hm_ctx *ctx, uint64_t *out, int32_t n);

@@ -22,7 +22,8 @@ vp = ctypes.c_void_p
 class HmStats(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("bfs_launches", ctypes.c_int64), ("bfs_ms", ctypes.c_double),
                 ("bfs_levels", ctypes.c_int64), ("bfs_batches", ctypes.c_int64),
-                ("bfs_model_bytes", ctypes.c_double)]
+                ("bfs_model_bytes", ctypes.c_double), ("bfs_row_commits", ctypes.c_int64),
+                ("bfs_csr_bytes", ctypes.c_double)]
 
 
 # name -> (restype, argtypes); must match include/hm.h (tests/test_abi.py checks the names)

@@ -450,8 +450,8 @@ hm_status hm_sync(hm_ctx *ctx) {
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(out, HM_EINVAL, "null out");
-    unsigned long long dv[3] = {0, 0, 0};
-    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long dv[5] = {0, 0, 0, 0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 40, cudaMemcpyDeviceToHost, ctx->stream));
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto &pe : ctx->pending) {
         float ms = 0.f;
@@ -467,6 +467,8 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     out->bfs_levels = (int64_t)dv[0];
     out->bfs_batches = (int64_t)dv[1];
     out->bfs_model_bytes = (double)dv[2];
+    out->bfs_row_commits = (int64_t)dv[3];
+    out->bfs_csr_bytes = (double)dv[4];
     if (reset) {
         ctx->stats = Stats();
         HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));

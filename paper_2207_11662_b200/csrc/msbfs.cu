@@ -47,7 +47,7 @@
 // Rows of degree > heavy_deg (R-MAT hubs) are cut into items of BFS_HEAVY_CHUNK
 // arcs that whole CTAs claim after their light units (heavy_items, out of line;
 // the last item of a row commits it).  The level barrier is one atomic per CTA on
-// a per-parity counter that also carries the level's any-change count.
+// per-parity counters that also sum the level's changed rows (the frontier size).
 //
 // (Variants measured and not kept -- two interleaved batch streams with split grid
 // barriers, half-CTA stream parts, a warp-wide pipelined item stream, per-CTA owned
@@ -159,7 +159,9 @@ struct Smem {
     int hi;
     int next;                       // next group to claim in this CTA's range
     int flag;
-    unsigned lb[4];              // fused level barrier (thread 0): expected arrivals, seen any-counts per parity
+    unsigned long long lb[4];    // fused level barrier (thread 0): expected arrivals [p], changed rows seen [2 + p]
+    int nchg;                    // rows this CTA changed in the current level
+    long long nlast;             // rows the whole grid changed in the previous level (the frontier size)
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
     int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
@@ -226,7 +228,7 @@ __device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglon
 // CTAs), each item's arcs split over the CTA's teams of T = W/2 lanes.  A row of several items ORs its partial rows into hacc; the last item to
 // arrive commits.  Returns whether this thread committed a change.
 template <int W, int BLOCK, bool WT>
-__device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+__device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                          const int2 *__restrict__ cinfo, const int32_t *__restrict__ heavy,
                                          const int32_t *__restrict__ hstart, unsigned long long *hacc, int32_t *hcnt,
                                          uint32_t *done, uint16_t *K, uint64_t *S, int32_t *hclaim, ulonglong2 *s_red_,
@@ -243,7 +245,7 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
     const int tl = lane % T;
     const int tbase = lane - tl;
     const unsigned tmask = ((T == 32) ? FULL : ((1u << T) - 1u)) << tbase;
-    bool any = false;
+    int ncommit = 0;                    // rows this thread committed (changed)
     __shared__ int sm_hh;               // heavy row of the current item
     __shared__ int sm_hlast;            // this CTA completed the heavy row (last item to arrive)
     __shared__ int sm_it;               // claimed item (hclaim: dynamic claims)
@@ -366,13 +368,13 @@ __device__ __noinline__ bool heavy_items(const int32_t *__restrict__ row_ptr, co
                     if (d & 1) atomicOr(&par[v >> 5], vbit);
                     else atomicAnd(&par[v >> 5], ~vbit);
                     if (kn + ((j >= 0 && j < nb) ? 1 : 0) == nb) atomicOr(&done[v >> 5], vbit);
-                    any = true;
+                    ++ncommit;
                 }
             }
         }
         __syncthreads();
     }
-    return any;
+    return ncommit;
 }
 
 // W words per row, TL lanes per light row, GD gathers in flight per lane, MINB CTAs per SM
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     Prof pf;
     PROF_INIT(pf);
     (void)pf;
-    if (threadIdx.x < 4) sm.lb[threadIdx.x] = 0u;
+    if (threadIdx.x < 4) sm.lb[threadIdx.x] = 0ull;
 
     for (int64_t base = 0; base < n_giant; base += B) {
         if (a.nshards > 1 && (int)((base / B) % a.nshards) != a.shard) continue;   // another shard's batch
@@ -513,8 +515,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             if (HV && gtid == 0 && a.hclaim) a.hclaim[(d + 1) % 3] = 0;   // next level's claims
             // stage the two previous change bitmaps in shared memory
             const uint32_t *chp_s = chp;
-            if (threadIdx.x == 0)
+            if (threadIdx.x == 0) {
                 sm.next = a.interleave ? 0 : (int)(((int64_t)blockIdx.x * (ngroups << a.unit_shift)) / gridDim.x);
+                sm.nchg = 0;
+            }
             if (a.chg_smem) {
                 const int nw4 = (int)((ngroups + 3) >> 2);
                 uint4 *d0 = s_dyn;
@@ -532,12 +536,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
             __syncthreads();
 #endif
-            bool any = false;
+            int nchg = 0;                 // rows changed by this thread (lane 0 of a unit / heavy committer)
 
             // ---- heavy rows (heavy_items): items of BFS_HEAVY_CHUNK arcs, claimed after the light
             // units (below); HM_HEAVY_DYN 0 deals them round-robin here instead
             if (HV && !HM_HEAVY_DYN && n_items > 0)
-                any = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
+                nchg = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                 a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
                                                 hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn);
             PROF_MARK(pf, 1);
@@ -737,7 +741,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         atomicOr(&a.has[g], chg_bits);
                         if (d & 1) atomicOr(&a.par[g], chg_bits);
                         else atomicAnd(&a.par[g], ~chg_bits);
-                        any = true;
+                        nchg += __popc(chg_bits);
                     }
                     if (done_bits) atomicOr(&a.done[g], done_bits);
                 }
@@ -754,13 +758,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             // holding a hub no longer finishes last; C4 layers -5 %, C3 -6 % against dealing them
             // round-robin before the light units; compiling both placements in is slower than either)
             if (HV && HM_HEAVY_DYN && n_items > 0)
-                any |= heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
+                nchg += heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                  a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
                                                  n_heavy, hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn,
                                                  chn);
+            // rows changed by this CTA: warp sums, one shared atomic per warp
+            nchg = __reduce_add_sync(FULL, nchg);
+            if (lane == 0 && nchg) atomicAdd(&sm.nchg, nchg);
+            __syncthreads();
+            const int nchg_cta = sm.nchg;
             // one flag write per CTA (same-address stores from every group serialise in L2)
-            const int any_cta = __syncthreads_or(any);
-            if (any_cta && threadIdx.x == 0 && !a.lbar) a.flags[d % 3] = 1;
+            if (nchg_cta && threadIdx.x == 0 && !a.lbar) a.flags[d % 3] = 1;
 #ifdef HM_MSBFS_PROF
             if (pf.on && threadIdx.x == 0 && a.dbgc) {
                 atomicAdd(a.dbgc + 8202, (unsigned long long)s_tmin << 4);
@@ -770,44 +778,49 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 #endif
             PROF_MARK(pf, 6);
             if (a.lbar) {
-                // level barrier with the any-change flag folded in: each CTA adds
-                // 1 | any << 32 to the level parity's counter; the barrier is complete at
-                // grid arrivals, and the high word grew iff some CTA saw a change.  (The
-                // next arrival on this parity needs every CTA past the next level, so the
-                // value read here is final for level d.)
+                // level barrier that also sums the level's changed rows: each CTA adds its count
+                // to the parity's change counter, then (after a fence) 1 to the parity's arrival
+                // counter; once all grid arrivals are seen, the change counter holds every CTA's
+                // count.  64-bit counters, never reset within a launch.  (The next arrival on
+                // this parity needs every CTA past the next level, so what is read is final.)
                 if (threadIdx.x == 0) {
                     const int p = d & 1;
-                    const unsigned long long add = 1ull | ((unsigned long long)(any_cta ? 1u : 0u) << 32);
+                    if (nchg_cta) atomicAdd(a.lbar + 2 + p, (unsigned long long)nchg_cta);
                     __threadfence();
-                    atomicAdd(a.lbar + p, add);
-                    // arrivals expected on this parity: grid x (its levels so far)
-                    const unsigned expect = sm.lb[p] + gridDim.x;
+                    atomicAdd(a.lbar + p, 1ull);
+                    const unsigned long long expect = sm.lb[p] + gridDim.x;
                     sm.lb[p] = expect;
                     unsigned long long v;
                     while (true) {
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.lbar + p) : "memory");
-                        if ((int)((unsigned)(v & 0xffffffffull) - expect) >= 0) break;
+                        if (v >= expect) break;
                         __nanosleep(20);
                     }
-                    const unsigned hiw = (unsigned)(v >> 32);
-                    sm.flag = (hiw != sm.lb[2 + p]) ? 1 : 0;
-                    sm.lb[2 + p] = hiw;
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.lbar + 2 + p) : "memory");
+                    sm.nlast = (long long)(v - sm.lb[2 + p]);
+                    sm.flag = (v != sm.lb[2 + p]) ? 1 : 0;
+                    sm.lb[2 + p] = v;
                     __threadfence();
                 }
                 __syncthreads();
             } else {
                 grid.sync();
-                if (threadIdx.x == 0) sm.flag = *((volatile int32_t *)(a.flags + (d % 3)));
+                if (threadIdx.x == 0) {
+                    sm.flag = *((volatile int32_t *)(a.flags + (d % 3)));
+                    sm.nlast = -1;                                   // unknown without the counting barrier
+                }
                 __syncthreads();
             }
             PROF_MARK(pf, 7);
             const int fv = sm.flag;
+            if (gtid == 0 && sm.nlast > 0) a.counters[3] += (unsigned long long)sm.nlast;   // row commits
             if (a.dbgc && gtid == 0) {
                 unsigned long long now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
                 const int di = d < 4095 ? d : 4095;
                 a.dbgc[di] += 1ull;
                 a.dbgc[4096 + di] += now - t_prev;
+                if (sm.nlast > 0) a.dbgc[12288 + di] += (unsigned long long)sm.nlast;   // rows changed at d
                 t_prev = now;
             }
             if (fv == 0) break;
@@ -819,6 +832,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             const unsigned long long arcs = (unsigned long long)a.row_ptr[hi];
             a.counters[2] += (unsigned long long)d *
                              (4ull * (hi + 1) + 4ull * arcs + 2ull * 8ull * W * (unsigned long long)hi);
+            a.counters[4] += (unsigned long long)d * (4ull * (hi + 1) + 4ull * arcs);   // CSR bytes per level
         }
     }
     PROF_FLUSH(pf, a.dbgc);
