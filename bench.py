@@ -468,7 +468,7 @@ def measured_traffic(args):
     """roofline traffic: DRAM bytes per MS-BFS launch from the committed ncu capture
     (tools/ncu_traffic.py) when it was taken on this config, batch width, L2 policy and MS-BFS source."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_msbfs_traffic.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*msbfs_traffic*.json")))
     sd = src_digest()
     for f in reversed(files):
         try:

@@ -848,7 +848,7 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     const int minb = blocks_per_sm == 1 ? 1 : 2;
     // gathers in flight per lane: 4 at W = 64 with 2 CTAs/SM (round 2, visited-set rows: C5 layer
     // 68.8 -> 64.8 ms, AND 62.2 -> 58.6 ms against 2)
-    if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : (vec == 2 ? 4 : 2));
+    if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : (vec == 2 && W == 64 ? 4 : 2));
 #define HM_MSBFS_CASE(w, tl, gd, mb)                                                                     \
     case ((w * 100 + tl) * 100 + gd * 10 + mb):                                                          \
         kern = a.tw ? (const void *)msbfs_kernel<w, tl, gd, mb, true> : (const void *)msbfs_kernel<w, tl, gd, mb, false>; \

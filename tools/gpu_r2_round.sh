@@ -1,0 +1,24 @@
+# round-2 artifacts on one B200: GPU tests, smoke, ncu traffic of the MS-BFS launches, bench (ours +
+# reference arm), ncu launch list of the bench command
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+if [ -z "$NO_TESTS" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gputests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/gputests.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+fi
+CFG=${CFG:-C5}
+P="python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
+$P > gpurun_out/plain3.log 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none \
+      -k regex:msbfs -c ${NCU_C:-4} -o gpurun_out/msbfs_traffic -f $P > gpurun_out/ncu_traffic.log 2>&1
+echo "ncu traffic rc=$?"
+python tools/ncu_traffic.py gpurun_out/msbfs_traffic.ncu-rep gpurun_out/r2_msbfs_traffic_$CFG.json $CFG 64 11 && \
+  cp gpurun_out/r2_msbfs_traffic_$CFG.json profiles/
+timeout 900 python bench.py --config $CFG ${BENCH_ARGS} > gpurun_out/bench_$CFG.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/bench_$CFG.log | cut -c1-600
+[ -n "$NO_REF" ] || { timeout 900 python bench.py --config $CFG --impl reference > gpurun_out/bench_ref_$CFG.log 2>&1; echo "ref rc=$?"; }
+[ -n "$NO_NCU" ] && exit 0
+CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+$CMD > gpurun_out/plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_list.log 2>&1
+echo "ncu list rc=$?"
