@@ -40,54 +40,92 @@ def log(*a):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: an NVML polling
+    thread (1 ms period, so even a few-ms region has samples); nvidia-smi -lms 100 if NVML is missing."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
     def __init__(self, index):
         self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.mx = None
+        self._stop = threading.Event()
+        self.t = None
+        self.nv = None
         self.proc = None
-        self.lines = []
+
+    def _handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.nv, h = self._handle()
+            self.mx = float(self.nv.nvmlDeviceGetMaxClockInfo(h, self.nv.NVML_CLOCK_SM))
+
+            def poll():
+                while True:
+                    self.samples.append(float(self.nv.nvmlDeviceGetClockInfo(h, self.nv.NVML_CLOCK_SM)))
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for name, bit in self.REASONS:
+                        if r & bit:
+                            self.reasons.add(name)
+                    if self._stop.wait(0.001):
+                        break
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
+        try:
+            fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                      "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.lines = []
+            self.t = threading.Thread(target=lambda: [self.lines.append(ln.strip()) for ln in self.proc.stdout],
+                                      daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
-
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 8:
-                continue
+        if self.nv is not None:
+            self._stop.set()
+            self.t.join(timeout=5)
+            src = "nvml (1 ms polling)"
+        elif self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(p[0]))
-                mx = float(p[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, p[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            for ln in self.lines:
+                p = [x.strip() for x in ln.split(",")]
+                try:
+                    self.samples.append(float(p[0]))
+                    self.mx = float(p[1])
+                except (ValueError, IndexError):
+                    continue
+                for (name, _), v in zip(self.REASONS, p[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(name)
+            src = "nvidia-smi -lms 100"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no NVML / nvidia-smi"], "samples": 0}
+        sm = self.samples
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": src}
 
 
 # ---------------------------------------------------------------------------
@@ -120,9 +158,9 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    dev = local_rank
+    dev = 0 if args.same_device else local_rank
     torch.cuda.set_device(dev)
-    h = build_config(args.config)
+    h = build_config(args.config, V=args.V)
     V, K = h.V, h.K
     ctx = Context(dev)
     s = ctx.stream
@@ -203,6 +241,40 @@ def run_ours(args, rank, world, local_rank):
     ctx.sync()
     ctx.stats(reset=True)
 
+    # ---- CUDA graph of the step (when no library call in it makes a host round trip: the probe step
+    # counts them).  Replaying the graph launches exactly the kernels of one eager step.
+    run_step = hot_step
+    graph_info = {"captured": False}
+    hot_step()
+    ctx.sync()
+    probe = ctx.stats(reset=True)
+    launches_per_step = probe["launches"]
+    graph_info["host_syncs_per_step"] = probe["host_syncs"]
+    if args.graph and not args.shard and probe["host_syncs"] == 0:
+        try:
+            ctx.set_param("timing", 0)
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=s):
+                hot_step()
+            torch.cuda.synchronize()
+            cap = ctx.stats(reset=True)
+            launches_per_step = cap["launches"]
+
+            def run_step():
+                with torch.cuda.stream(s):
+                    cg.replay()
+            run_step()
+            torch.cuda.synchronize()
+            graph_info = {"captured": True, "host_syncs_per_step": 0, "launches_captured": cap["launches"]}
+        except Exception as ex:       # keep the eager step
+            log(f"CUDA graph capture failed ({ex}); timing the eager step")
+            torch.cuda.synchronize()
+            run_step = hot_step
+            graph_info["capture_error"] = str(ex)[:200]
+        finally:
+            ctx.set_param("timing", 1)
+    ctx.stats(reset=True)
+
     # ---- timed (device-resident inputs)
     clk = ClockSampler(dev)
     if world > 1:
@@ -216,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        hot_step()
+        run_step()
         e1.record(s)
         times.append((e0, e1))
     torch.cuda.synchronize()
@@ -362,9 +434,16 @@ def run_ours(args, rank, world, local_rank):
             per_graph[name] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
         for g in ands:
             ctx.free_graph(g)
-    n_bfs = max(1, st["bfs_launches"])
-    bfs_ms_avg = st["bfs_ms"] / n_bfs
-    levels_per_launch = st["bfs_levels"] / n_bfs
+    if per_graph:                           # per-launch numbers from the eager per-graph pass
+        n_bfs = len(per_graph)
+        bfs_ms_avg = float(np.mean([v["ms"] for v in per_graph.values()]))
+        levels_per_launch = float(np.mean([v["levels"] for v in per_graph.values()]))
+        bfs_ms_step = float(sum(v["ms"] for v in per_graph.values()))
+    else:
+        n_bfs = max(1, st["bfs_launches"])
+        bfs_ms_avg = st["bfs_ms"] / n_bfs
+        levels_per_launch = st["bfs_levels"] / n_bfs
+        bfs_ms_step = st["bfs_ms"] / args.steps
     # headline: the dominant kernel, the plain MS-BFS launches of the layers (3 of the 4 launches of a
     # C5 step, ~75 % of it); algorithmic bytes = SURVEY §8(d) dense-level model of this algorithm,
     # accumulated by the kernel per batch:  L * (4 (rows + 1) + 4 arcs + 2 R rows),  R = 8 W bytes
@@ -391,9 +470,8 @@ def run_ours(args, rank, world, local_rank):
             "per_graph_note": "model = dense-level bytes; compulsory = 2 R x rows actually changed + CSR per level; "
                               "ncu_dram = dram__bytes_read+write of the same launch (ncu, serialised, cold cache)",
             "levels_per_launch": levels_per_launch, "bfs_ms_per_launch_all": bfs_ms_avg,
-            "bfs_share_of_step": st["bfs_ms"] / max(total_ms, 1e-9),
+            "bfs_share_of_step": bfs_ms_step / max(ms_per_step, 1e-9),
             "fused_graphs": 1 if (not args.fused) else len(arcs)}
-    launches_per_step = st["launches"] / args.steps
 
     line = {
         "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",
@@ -408,11 +486,31 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"batch-shard{world}+nccl-allreduce(S)" if args.shard else f"replicas{world}"},
         "s_per_homln": ms_per_step / 1e3,
         "e2e": e2e, "roofline": roof, "clocks": clocks, "gpu_launches": int(round(launches_per_step)),
+        "cuda_graph": graph_info,
         "breakdown_ms": breakdown,
         "accuracy_vs_gt_topk": accuracy,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:      # the oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(h, args.cpu_seconds)
+    if args.dump:
+        # one more step through the same psi() (plain, fused or sharded + all-reduce), then every
+        # graph's results and every ranked list, for the parity tests
+        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        gids = list(range(len(h.layers))) + ands
+        psi(gids)
+        dump = {}
+        for g, name in zip(gids, [f"L{i}" for i in range(len(h.layers))] + ["AND" + "".join(map(str, T)) for T in h.subsets]):
+            for key, arr in ctx.closeness_results(g).items():
+                dump[f"{name}_{key}"] = arr
+        for T, g in zip(h.subsets, ands):
+            tag = "".join(map(str, T))
+            dump[f"gt_{tag}"] = ctx.topk_closeness(g, K)
+            dump[f"cc2_{tag}"] = ctx.compose("cc2", list(T), K)[0]
+            dump[f"cc1_{tag}"] = ctx.compose(cc1_name(T), list(T), K)[0]
+            dump[f"naive_{tag}"] = ctx.compose("naive", list(T), K)[0]
+            ctx.free_graph(g)
+        if rank == 0:
+            np.savez(args.dump, **dump)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -617,11 +715,20 @@ def main():
     ap.add_argument("--words", type=int, default=64)
     ap.add_argument("--hints", type=int, default=11, help="MS-BFS L2 eviction-priority bits (library bfs_hints)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time the eager step even when it could be captured in a CUDA graph")
     ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: split every graph's source batches over the ranks, NCCL all-reduce of S")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N > 1 (gloo: host-staged, for the 2-rank test on one GPU)")
+    ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (tests only)")
+    ap.add_argument("--V", type=int, default=None, help="scale the config to V vertices (tests only)")
+    ap.add_argument("--dump", default=None,
+                    help="after the run, rank 0 writes every graph's closeness results and every ranked list "
+                         "of one more step to this .npz (tests)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -632,8 +739,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(0 if args.same_device else local_rank)
+        dist.init_process_group(args.backend)
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -79,6 +79,10 @@ const char *hm_last_error(const hm_ctx *ctx);
  *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16, 8, 4 or 2; 0 = default: chosen from
  *                   the live rows per warp of the grid, 32 on C5-sized graphs)
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)
+ *   "bfs_td"      : direction optimisation (north_star; the BFS of PAPER.md:209): a level runs top-down --
+ *                   the frontier (rows changed at the previous level) marks its neighbours as candidates,
+ *                   then only candidate rows pull -- when frontier rows * bfs_td <= the batch's rows, else
+ *                   bottom-up over every row not yet complete; 0 = always bottom-up
  *   "bfs_chg_smem": 1 stages the per-level change bitmaps in shared memory, 0 (default) reads them via L1
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
  *   "bfs_dbg"     : debug: bit 1 (value 2) = per-level counters and times (hm_debug_counts);
@@ -265,6 +269,9 @@ typedef struct {
     int64_t bfs_row_commits;  /* rows changed, summed over levels and batches (each one own-row read and one
                                  8 W-byte row write: the compulsory state traffic); needs bfs_fbar = 1 */
     double bfs_csr_bytes;     /* CSR bytes of the same model: levels * (4 (rows + 1) + 4 arcs) per batch */
+    int64_t bfs_td_levels;    /* levels run top-down (frontier-driven candidate rows, parameter bfs_td) */
+    int64_t host_syncs;       /* host round trips (stream synchronisations) made inside library calls: a
+                                 sequence of calls with none can be captured in a CUDA graph */
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
 

@@ -569,14 +569,14 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         int32_t h_rows = 0;
         HM_CUDA(cudaMemcpyAsync(&h_rows, cntb.p, 4, cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaMemcpyAsync(&h_heavy, scalars + 3, 4, cudaMemcpyDeviceToHost, s));
-        HM_CUDA(cudaStreamSynchronize(s));
+        host_sync(ctx);
         frows = (int64_t)h_rows + 32;
         if (frows > V) frows = V;
         if (frows < 32) frows = 32;
     }
     const size_t bmw = (((size_t)(V + 31) / 32) + 4) & ~(size_t)3;   // multiple of 4 words (16-B rows for uint4 copies)
     Buf F0((size_t)frows * rowb, s), F1((size_t)frows * rowb, s);
-    Buf bms(bmw * 6 * 4, s), Srel((size_t)V * 8, s), Kb((size_t)V * 2 + 16, s), flags(128, s);
+    Buf bms(bmw * 8 * 4, s), Srel((size_t)V * 8, s), Kb((size_t)V * 2 + 16, s), flags(128, s);
     HM_CUDA(cudaMemsetAsync(Srel.p, 0, Srel.bytes, s));
     HM_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, s));
     BfsArgs a;
@@ -622,6 +622,9 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.done = bm + 3 * bmw;
     a.has = bm + 4 * bmw;
     a.par = bm + 5 * bmw;
+    a.cand[0] = bm + 6 * bmw;
+    a.cand[1] = bm + 7 * bmw;
+    a.td_div = ctx->params.bfs_td;
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
     a.hints = ctx->params.bfs_hints;

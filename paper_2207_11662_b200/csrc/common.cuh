@@ -73,7 +73,9 @@ struct Graph {
     bool alive = false;
     bool is_layer = false;
     int32_t V = 0;
-    int64_t nnz = 0;          // arcs = 2 m
+    int64_t nnz = 0;          // arcs = 2 m (an upper bound while !nnz_exact: AND aggregates, whose exact
+                              // count stays on the device in row_ptr[V] until exact_nnz() reads it)
+    bool nnz_exact = true;
     Buf row_ptr, col;         // CSR, rows ascending
     // cached Psi results (valid when has_results)
     bool has_results = false;
@@ -95,12 +97,14 @@ struct Params {
     int bfs_unit = 0;          // MS-BFS light-path rows per work unit (0 = auto by rows per warp; 32 ... 2)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level
+    int bfs_td = 0;            // direction switch: top-down levels when frontier * bfs_td <= rows (0 = off)
     int timing = 0;
     int bfs_dbg = 0;
 };
 
 struct Stats {
     int64_t launches = 0;
+    int64_t host_syncs = 0;   // host round trips (stream synchronisations) inside library calls
     int64_t bfs_launches = 0;
     double bfs_ms = 0;
 };
@@ -126,6 +130,12 @@ struct hm_ctx {
 namespace hm {
 
 inline void count_launch(hm_ctx *ctx, int n = 1) { ctx->stats.launches += n; }
+
+// a host round trip inside a library call (counted: a step without any can be captured in a CUDA graph)
+inline void host_sync(hm_ctx *ctx) {
+    ++ctx->stats.host_syncs;
+    HM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
 
 // Row of arc j of a CSR (row_ptr[0..V], V >= 1, 0 <= j < row_ptr[V]): the largest u with
 // row_ptr[u] <= j.  Arc-parallel kernels use it so that a hub row is spread over many threads
@@ -153,6 +163,7 @@ inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148LL * 32) {
 }
 
 Graph &graph(hm_ctx *ctx, int32_t g);                 // throws ESTATE
+int64_t exact_nnz(hm_ctx *ctx, Graph &G);             // reads row_ptr[V] (one host round trip) if not known
 bool is_device_ptr(const void *p);
 void copy_out(hm_ctx *ctx, void *dst, const void *dsrc, size_t bytes);  // host or device dst
 

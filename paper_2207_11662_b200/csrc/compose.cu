@@ -95,11 +95,12 @@ __global__ void k_cc1_main(LayerPtrs L, int V, int64_t nnz0, const double *ratio
                            int32_t *icnt, uint32_t *R, int pass) {
     const double avg_and = *avg_and_p;
     const int64_t n = nnz0 > V ? nnz0 : V;
+    const int64_t na = L.rp[0][V];     // layer 0's arcs (nnz0 may be an upper bound: an AND graph)
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
         if (pass == 1 && j < V && cc1_common(L, (int)j)) atomicOr(&R[j >> 5], 1u << (j & 31));
         bool in = false;
         int u = -1;
-        if (j < nnz0) {
+        if (j < na) {
             u = csr_row_of(L.rp[0], V, j);
             if (cc1_common(L, u) && (pass == 0 || icnt[u] > 1)) {
                 const int v = L.cl[0][j];
@@ -333,7 +334,7 @@ void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t
     }
     std::vector<int32_t> h((size_t)K + 1);
     HM_CUDA(cudaMemcpyAsync(h.data(), d_ids, (size_t)(K + 1) * 4, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     const int32_t nR = h[K];
     const int32_t Kout = nR < K ? nR : K;
     if (dev_ids) {

@@ -82,7 +82,12 @@ struct AggIn {
 __global__ void k_and_keep(AggIn in, int32_t V, int64_t nd, int32_t *keep) {
     const int32_t *rpd = in.rp[in.drv];
     const int32_t *cld = in.cl[in.drv];
+    const int64_t na = rpd[V];         // the driver's arcs (nd may be an upper bound: an AND input)
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += (int64_t)gridDim.x * blockDim.x) {
+        if (j >= na) {
+            keep[j] = 0;
+            continue;
+        }
         const int u = csr_row_of(rpd, V, j);
         const int v = cld[j];
         bool ok = true;
@@ -135,7 +140,7 @@ int64_t csr_from_sorted_keys(hm_ctx *ctx, const uint64_t *d_sorted, int64_t n, i
     HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.as<int32_t>(), pos.as<int32_t>(), n + 1, s));
     int32_t nnz32 = 0;
     HM_CUDA(cudaMemcpyAsync(&nnz32, pos.as<int32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     const int64_t nnz = nnz32;
     Buf ukeys((size_t)(nnz > 0 ? nnz : 1) * 8, s);
     k_compact_keys<<<g, TB, 0, s>>>(d_sorted, flag.as<int32_t>(), pos.as<int32_t>(), n, ukeys.as<uint64_t>());
@@ -164,6 +169,21 @@ void sort_keys(hm_ctx *ctx, Buf &keys, Buf &sorted, int64_t n, int end_bit) {
                                            end_bit, s));
     count_launch(ctx, 4);
 }
+
+}  // namespace
+
+int64_t exact_nnz(hm_ctx *ctx, Graph &G) {
+    if (!G.nnz_exact) {
+        int32_t n = 0;
+        HM_CUDA(cudaMemcpyAsync(&n, G.row_ptr.as<int32_t>() + G.V, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        host_sync(ctx);
+        G.nnz = n;
+        G.nnz_exact = true;
+    }
+    return G.nnz;
+}
+
+namespace {
 
 __global__ void k_degrees(const int32_t *row_ptr, int32_t V, int32_t *deg) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
@@ -201,7 +221,7 @@ void build_csr(hm_ctx *ctx, int32_t V, const int32_t *edges, int64_t m, Graph &G
     }
     int32_t h_bad = 0;
     HM_CUDA(cudaMemcpyAsync(&h_bad, bad.p, 4, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     HM_REQUIRE(!h_bad, HM_ERANGE, "edge endpoint outside [0, V)");
     if (n > 0) sort_keys(ctx, keys, sorted, n, 32 + nbits((uint64_t)V));
     const int64_t nnz = csr_from_sorted_keys(ctx, sorted.as<uint64_t>(), n, V, G);
@@ -234,12 +254,12 @@ void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, 
         HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), nd + 1, s));
         Buf tmp(tb, s);
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, keep.as<int32_t>(), pos.as<int32_t>(), nd + 1, s));
-        int32_t nnz = 0;
-        HM_CUDA(cudaMemcpyAsync(&nnz, pos.as<int32_t>() + nd, 4, cudaMemcpyDeviceToHost, s));
-        HM_CUDA(cudaStreamSynchronize(s));
+        // no host round trip: the output is sized by the driver's arcs (an upper bound; the
+        // exact count stays on the device in row_ptr[V] and is read only when a caller asks)
         out.V = V;
-        out.nnz = nnz;
-        out.col.alloc((size_t)(nnz > 0 ? nnz : 1) * 4, s);
+        out.nnz = nd;
+        out.nnz_exact = false;
+        out.col.alloc((size_t)(nd > 0 ? nd : 1) * 4, s);
         k_and_fill<<<ga, TB, 0, s>>>(a, V, nd, keep.as<int32_t>(), pos.as<int32_t>(), orp.as<int32_t>(),
                                      out.col.as<int32_t>());
         out.row_ptr = std::move(orp);
@@ -247,7 +267,7 @@ void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, 
         count_launch(ctx, 3);
     } else {
         std::vector<int64_t> off(r + 1, 0);
-        for (int i = 0; i < r; ++i) off[i + 1] = off[i] + in[i]->nnz;
+        for (int i = 0; i < r; ++i) off[i + 1] = off[i] + exact_nnz(ctx, *in[i]);
         const int64_t n = off[r];
         HM_REQUIRE(n < (int64_t)INT32_MAX, HM_ERANGE, "OR aggregate too large for an int32 CSR");
         Buf doff((size_t)(r + 1) * 8, s), keys((size_t)(n > 0 ? n : 1) * 8, s), sorted((size_t)(n > 0 ? n : 1) * 8, s);
@@ -257,7 +277,7 @@ void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, 
         count_launch(ctx);
         if (n > 0) sort_keys(ctx, keys, sorted, n, 32 + nbits((uint64_t)V));
         csr_from_sorted_keys(ctx, sorted.as<uint64_t>(), n, V, out);
-        HM_CUDA(cudaStreamSynchronize(s));   // host vector `off` lifetime
+        host_sync(ctx);   // host vector `off` lifetime
     }
     out.alive = true;
     out.is_layer = false;

@@ -31,7 +31,7 @@ void copy_out(hm_ctx *ctx, void *dst, const void *dsrc, size_t bytes) {
         HM_CUDA(cudaMemcpyAsync(dst, dsrc, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
         HM_CUDA(cudaMemcpyAsync(dst, dsrc, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-        HM_CUDA(cudaStreamSynchronize(ctx->stream));
+        host_sync(ctx);
     }
 }
 
@@ -154,6 +154,9 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value == 0 || value == 4 || value == 8 || value == 16 || value == 32, HM_EINVAL,
                    "bfs_team must be 0 (default), 4, 8, 16 or 32 (and at most words/2)");
         ctx->params.bfs_team = (int)value;
+    } else if (n == "bfs_td") {
+        HM_REQUIRE(value >= 0 && value <= (1 << 20), HM_EINVAL, "bfs_td must be in [0, 2^20]");
+        ctx->params.bfs_td = (int)value;
     } else if (n == "bfs_chg_smem") {
         ctx->params.bfs_chg_smem = value ? 1 : 0;
     } else if (n == "bfs_dbg") {
@@ -196,7 +199,7 @@ hm_status hm_graph_info(hm_ctx *ctx, int32_t g, int32_t *V, int64_t *m_undirecte
     HM_API_BEGIN(ctx)
     Graph &G = graph(ctx, g);
     if (V) *V = G.V;
-    if (m_undirected) *m_undirected = G.nnz / 2;
+    if (m_undirected) *m_undirected = exact_nnz(ctx, G) / 2;
     if (d_row_ptr) *d_row_ptr = G.row_ptr.as<int32_t>();
     if (d_col) *d_col = G.col.as<int32_t>();
     HM_API_END(ctx)
@@ -206,7 +209,7 @@ hm_status hm_graph_csr(hm_ctx *ctx, int32_t g, int32_t *row_ptr, int32_t *col) {
     HM_API_BEGIN(ctx)
     Graph &G = graph(ctx, g);
     copy_out(ctx, row_ptr, G.row_ptr.p, (size_t)(G.V + 1) * 4);
-    copy_out(ctx, col, G.col.p, (size_t)G.nnz * 4);
+    copy_out(ctx, col, G.col.p, (size_t)exact_nnz(ctx, G) * 4);
     HM_API_END(ctx)
 }
 
@@ -302,7 +305,7 @@ hm_status hm_closeness_combine(hm_ctx *ctx, int32_t g, const uint64_t *S_total) 
         Buf tmp(V * 8, ctx->stream);
         HM_CUDA(cudaMemcpyAsync(tmp.p, S_total, V * 8, cudaMemcpyHostToDevice, ctx->stream));
         closeness_combine(ctx, G, tmp.as<uint64_t>());
-        HM_CUDA(cudaStreamSynchronize(ctx->stream));   // the host buffer may be reused on return
+        host_sync(ctx);   // the host buffer may be reused on return
     }
     HM_API_END(ctx)
 }
@@ -329,7 +332,7 @@ hm_status hm_cc_nodes(hm_ctx *ctx, int32_t g, uint32_t *bitmap, int32_t *count, 
     const char *base = G.ch.as<char>() + ((nbw * 4 + 7) / 8) * 8;
     struct { double mu; int32_t cnt; int32_t pad; } h;
     HM_CUDA(cudaMemcpyAsync(&h, base, 12, cudaMemcpyDeviceToHost, ctx->stream));
-    HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    host_sync(ctx);
     if (count) *count = h.cnt;
     if (mean) *mean = h.mu;
     HM_API_END(ctx)
@@ -396,7 +399,7 @@ hm_status hm_set_metrics(hm_ctx *ctx, int32_t V, const int32_t *est_ids, int64_t
     set_metrics(ctx, V, de, n_est, dg, n_gt, res.as<double>(), d_bad);
     double h[8];
     HM_CUDA(cudaMemcpyAsync(h, res.p, sizeof h, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     int32_t bad;
     memcpy(&bad, &h[7], 4);
     HM_REQUIRE(!bad, HM_ERANGE, "vertex id outside [0, V)");
@@ -425,7 +428,7 @@ hm_status hm_exact_mean(hm_ctx *ctx, const double *x, int64_t n, const uint8_t *
     exact_mean(ctx, dx, n, dm, res.as<double>(), d_cnt_bad, d_cnt_bad + 1);
     struct { double mu; int32_t cnt, bad; } h;
     HM_CUDA(cudaMemcpyAsync(&h, res.p, 16, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     HM_REQUIRE(!h.bad, HM_EINVAL, "a selected value is negative, inf or nan");
     *mean_out = h.mu;
     if (count_out) *count_out = h.cnt;
@@ -450,8 +453,8 @@ hm_status hm_sync(hm_ctx *ctx) {
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(out, HM_EINVAL, "null out");
-    unsigned long long dv[5] = {0, 0, 0, 0, 0};
-    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 40, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long dv[6] = {0, 0, 0, 0, 0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 48, cudaMemcpyDeviceToHost, ctx->stream));
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto &pe : ctx->pending) {
         float ms = 0.f;
@@ -462,6 +465,7 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     }
     ctx->pending.clear();
     out->launches = ctx->stats.launches;
+    out->host_syncs = ctx->stats.host_syncs;
     out->bfs_launches = ctx->stats.bfs_launches;
     out->bfs_ms = ctx->stats.bfs_ms;
     out->bfs_levels = (int64_t)dv[0];
@@ -469,6 +473,7 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     out->bfs_model_bytes = (double)dv[2];
     out->bfs_row_commits = (int64_t)dv[3];
     out->bfs_csr_bytes = (double)dv[4];
+    out->bfs_td_levels = (int64_t)dv[5];
     if (reset) {
         ctx->stats = Stats();
         HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));

@@ -159,9 +159,10 @@ struct Smem {
     int hi;
     int next;                       // next group to claim in this CTA's range
     int flag;
-    unsigned long long lb[4];    // fused level barrier (thread 0): expected arrivals [p], changed rows seen [2 + p]
+    unsigned long long lb[4];    // counting barrier (thread 0): expected arrivals [p], changed rows seen [2 + p]
+    unsigned long long epoch;    // counting barriers passed (thread 0); parity p = epoch & 1
     int nchg;                    // rows this CTA changed in the current level
-    long long nlast;             // rows the whole grid changed in the previous level (the frontier size)
+    long long nlast;             // rows the whole grid changed before the last counting barrier
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
     int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
@@ -223,6 +224,63 @@ __device__ __forceinline__ void st_row(uint64_t *F, int v, int l, const ulonglon
     for (int q = 0; q < VEC; ++q) st2p(F + (size_t)v * W + 2 * (q * TL + l), r[q], pol);
 }
 
+// Grid barrier that also sums a per-CTA count (thread 0 only; the caller __syncthreads() after).
+// Each CTA adds its count to the epoch parity's count counter, then (after a fence) 1 to the
+// parity's arrival counter; once all grid arrivals are seen, the count counter holds every CTA's
+// count: sm.nlast = the grid's total for this barrier, sm.flag = (total != 0).  64-bit counters,
+// never reset within a launch.  (The next arrival on this parity needs every CTA past the next
+// barrier, which needs this CTA's arrival there, so what is read here is final.)
+template <class SM>
+__device__ __forceinline__ void count_barrier(unsigned long long *lbar, SM &sm, int add) {
+    const int p = (int)(sm.epoch & 1ull);
+    ++sm.epoch;
+    if (add) atomicAdd(lbar + 2 + p, (unsigned long long)add);
+    __threadfence();
+    atomicAdd(lbar + p, 1ull);
+    const unsigned long long expect = sm.lb[p] + gridDim.x;
+    sm.lb[p] = expect;
+    unsigned long long v;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lbar + p) : "memory");
+        if (v >= expect) break;
+        __nanosleep(20);
+    }
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lbar + 2 + p) : "memory");
+    sm.nlast = (long long)(v - sm.lb[2 + p]);
+    sm.flag = (v != sm.lb[2 + p]) ? 1 : 0;
+    sm.lb[2 + p] = v;
+    __threadfence();
+}
+
+// Top-down discovery for a sparse level (direction optimisation): every row that changed at
+// d-1 (the frontier, bitmap chp) marks its neighbours that are not done as candidates; the
+// level's pull step then visits candidate rows only.  Warp per 32-row frontier group, striding
+// over the group's packed arcs (row index in the low 5 bits): coalesced and independent loads.
+__device__ __noinline__ void td_discover(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                         const uint32_t *chp, const uint32_t *done, uint32_t *cand, int hi,
+                                         int64_t ngroups, int64_t gwarp, int64_t nwarps) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+        const uint32_t fw = chp[g];
+        if (!fw) continue;                                   // warp-uniform
+        const int r0 = (int)(g * 32) + __ffs(fw) - 1;        // first and last frontier row of the group
+        const int r1 = (int)(g * 32) + 32 - __clz(fw);
+        const int A0 = row_ptr[r0], A1 = row_ptr[r1 < hi ? r1 : hi];
+        for (int j0 = A0; j0 < A1; j0 += 32 * 4) {
+            int x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = (j0 + 32 * q + lane < A1) ? col[j0 + 32 * q + lane] : -1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (x[q] >= 0 && ((fw >> (x[q] & 31)) & 1u)) {
+                    const int v = x[q] >> 5;
+                    if (!bit_of(done, v)) atomicOr(&cand[v >> 5], 1u << (v & 31));
+                }
+            }
+        }
+    }
+}
+
 // Heavy rows (degree > heavy_deg), out of line: items of BFS_HEAVY_CHUNK arcs (hstart: first item
 // of each heavy row), claimed from the level's counter hclaim (nullptr: dealt round-robin over the
 // CTAs), each item's arcs split over the CTA's teams of T = W/2 lanes.  A row of several items ORs its partial rows into hacc; the last item to
@@ -236,7 +294,7 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
                                  int hi, int n_giant, int64_t base, int d, const uint32_t *chp_s,
                                  uint32_t *has, uint32_t *par, const uint64_t *__restrict__ Fc,
                                  const uint64_t *F0, const uint64_t *F1, uint64_t *__restrict__ Fn,
-                                 uint32_t *chn) {
+                                 uint32_t *chn, const uint32_t *cand) {
     constexpr int T = W / 2;
     constexpr int TPB = BLOCK / T;
     constexpr int64_t B = 64 * W;
@@ -269,6 +327,7 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
         __syncthreads();                                         // sm_hh reused next item
         if (v >= hi) continue;                                   // block-uniform
         if (bit_of(done, v)) continue;                         // block-uniform
+        if (cand && !bit_of(cand, v)) continue;                // top-down level: not adjacent to the frontier
         const int rb = row_ptr[v] + (it - i0) * BFS_HEAVY_CHUNK;
         const int re = min(row_ptr[v + 1], rb + BFS_HEAVY_CHUNK);
         ulonglong2 acc = make_ulonglong2(0ull, 0ull);
@@ -432,6 +491,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     PROF_INIT(pf);
     (void)pf;
     if (threadIdx.x < 4) sm.lb[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) sm.epoch = 0ull;
 
     for (int64_t base = 0; base < n_giant; base += B) {
         if (a.nshards > 1 && (int)((base / B) % a.nshards) != a.shard) continue;   // another shard's batch
@@ -441,6 +501,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         const int64_t ngroups = (hi + 31) >> 5;
 
         // ---- level 0: sources of every component window (F_0); bitmaps and counts reset
+        int nsrc = 0;                                                // source rows (lane 0 counts its groups)
         for (int64_t g = gwarp; g < ngroups; g += nwarps) {
             const int v = (int)(g * 32 + lane);
             bool src = false, dn = false;
@@ -468,6 +529,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 a.chg[1][g] = 0u;     // written at level 1
                 a.has[g] = bs;        // only the sources hold a visited set, in buffer 0
                 a.par[g] = 0u;
+                a.cand[1][g] = 0u;    // level 1's top-down candidates (level d clears level d+1's)
+                nsrc += __popc(bs);
                 a.done[g] = bd;
             }
         }
@@ -485,7 +548,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 }
             }
         }
-        grid.sync();
+        if (a.lbar) {                                                // the level-0 frontier: the sources
+            if (threadIdx.x == 0) sm.nchg = 0;
+            __syncthreads();
+            nsrc = __reduce_add_sync(FULL, nsrc);
+            if (lane == 0 && nsrc) atomicAdd(&sm.nchg, nsrc);
+            __syncthreads();
+            if (threadIdx.x == 0) count_barrier(a.lbar, sm, sm.nchg);
+            __syncthreads();
+        } else {
+            grid.sync();
+            if (threadIdx.x == 0) sm.nlast = -1;
+        }
         if constexpr (WT) {
             if (threadIdx.x == 0) s_nb = 0;
             __syncthreads();
@@ -510,7 +584,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             const uint32_t *chp = a.chg[(d + 2) % 3];
             uint32_t *chn = a.chg[d % 3];
             uint32_t *chz = a.chg[(d + 1) % 3];
-            for (int64_t w = gtid; w < ngroups; w += nthreads) chz[w] = 0u;
+            uint32_t *cand_n = a.cand[(d + 1) & 1];
+            for (int64_t w = gtid; w < ngroups; w += nthreads) {
+                chz[w] = 0u;
+                cand_n[w] = 0u;                                  // level d+1's top-down candidates
+            }
             if (gtid == 0) a.flags[(d + 1) % 3] = 0;
             if (HV && gtid == 0 && a.hclaim) a.hclaim[(d + 1) % 3] = 0;   // next level's claims
             // stage the two previous change bitmaps in shared memory
@@ -526,7 +604,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 for (int i = threadIdx.x; i < nw4; i += BLOCK) d0[i] = s0[i];
                 chp_s = reinterpret_cast<const uint32_t *>(d0);
             }
+            // direction: top-down when the frontier (rows changed at d-1) is small against the batch's rows
+            const long long frontier = sm.nlast;
+            const bool td = a.td_div > 0 && a.lbar && frontier >= 0 && frontier * a.td_div <= (long long)hi;
+            const uint32_t *cand = td ? a.cand[d & 1] : nullptr;
             __syncthreads();
+            if (td) {
+                td_discover(a.row_ptr, a.col, chp_s, a.done, a.cand[d & 1], hi, ngroups, gwarp, nwarps);
+                __syncthreads();
+                if (threadIdx.x == 0) count_barrier(a.lbar, sm, 0);
+                __syncthreads();
+            }
             PROF_MARK(pf, 0);
 #ifdef HM_MSBFS_PROF
             const long long t_lvl0 = clock64();
@@ -543,7 +631,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             if (HV && !HM_HEAVY_DYN && n_items > 0)
                 nchg = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                 a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
-                                                hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn);
+                                                hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn,
+                                                cand);
             PROF_MARK(pf, 1);
 
             // ---- light rows: one warp per unit of 32 >> unit_shift rows of a 32-row group;
@@ -576,7 +665,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 const bool inunit = lane >= q0 && lane < q0 + ur;
                 const int rp = a.row_ptr[valid ? r : hi];
                 const int rlast = a.row_ptr[(int)(g * 32 + 32) < hi ? (int)(g * 32 + 32) : hi];
-                const uint32_t dword = a.done[g];
+                const uint32_t dword = a.done[g] | (td ? ~cand[g] : 0u);   // top-down: candidates only
                 const int rnext = __shfl_down_sync(FULL, rp, 1);
                 const int rend = (lane == 31) ? rlast : rnext;
                 const bool act = valid && inunit && !((dword >> lane) & 1u) && (rend - rp) <= heavy_deg;
@@ -761,7 +850,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 nchg += heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                  a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
                                                  n_heavy, hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn,
-                                                 chn);
+                                                 chn, cand);
             // rows changed by this CTA: warp sums, one shared atomic per warp
             nchg = __reduce_add_sync(FULL, nchg);
             if (lane == 0 && nchg) atomicAdd(&sm.nchg, nchg);
@@ -778,30 +867,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 #endif
             PROF_MARK(pf, 6);
             if (a.lbar) {
-                // level barrier that also sums the level's changed rows: each CTA adds its count
-                // to the parity's change counter, then (after a fence) 1 to the parity's arrival
-                // counter; once all grid arrivals are seen, the change counter holds every CTA's
-                // count.  64-bit counters, never reset within a launch.  (The next arrival on
-                // this parity needs every CTA past the next level, so what is read is final.)
-                if (threadIdx.x == 0) {
-                    const int p = d & 1;
-                    if (nchg_cta) atomicAdd(a.lbar + 2 + p, (unsigned long long)nchg_cta);
-                    __threadfence();
-                    atomicAdd(a.lbar + p, 1ull);
-                    const unsigned long long expect = sm.lb[p] + gridDim.x;
-                    sm.lb[p] = expect;
-                    unsigned long long v;
-                    while (true) {
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.lbar + p) : "memory");
-                        if (v >= expect) break;
-                        __nanosleep(20);
-                    }
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.lbar + 2 + p) : "memory");
-                    sm.nlast = (long long)(v - sm.lb[2 + p]);
-                    sm.flag = (v != sm.lb[2 + p]) ? 1 : 0;
-                    sm.lb[2 + p] = v;
-                    __threadfence();
-                }
+                if (threadIdx.x == 0) count_barrier(a.lbar, sm, nchg_cta);   // sm.nlast = rows changed at d
                 __syncthreads();
             } else {
                 grid.sync();
@@ -813,7 +879,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
             PROF_MARK(pf, 7);
             const int fv = sm.flag;
-            if (gtid == 0 && sm.nlast > 0) a.counters[3] += (unsigned long long)sm.nlast;   // row commits
+            if (gtid == 0) {
+                if (sm.nlast > 0) a.counters[3] += (unsigned long long)sm.nlast;   // row commits
+                if (td) a.counters[5] += 1ull;                                      // top-down levels
+            }
             if (a.dbgc && gtid == 0) {
                 unsigned long long now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
@@ -821,6 +890,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 a.dbgc[di] += 1ull;
                 a.dbgc[4096 + di] += now - t_prev;
                 if (sm.nlast > 0) a.dbgc[12288 + di] += (unsigned long long)sm.nlast;   // rows changed at d
+                if (td) a.dbgc[16384 + di] += 1ull;                                      // top-down at d
                 t_prev = now;
             }
             if (fv == 0) break;

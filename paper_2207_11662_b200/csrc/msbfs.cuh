@@ -35,10 +35,14 @@ struct BfsArgs {
     uint32_t *done;              // row bitmap: all sources of the row's window reached it
     uint32_t *has;               // row bitmap: the row holds a visited set in this batch
     uint32_t *par;               // row bitmap: parity of the level that last wrote the row (its buffer)
+    uint32_t *cand[2];           // top-down levels: rows adjacent to the frontier ("candidates"), by level parity
+    int td_div;                  // direction switch: a level runs top-down (frontier-driven candidate rows)
+                                 // when frontier rows * td_div <= the batch's rows; 0 = always bottom-up
     uint16_t *K;                 // [n_live] window sources reached so far in this batch (self excluded)
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
-    unsigned long long *counters;  // [0] levels, [1] batches
+    unsigned long long *counters;  // [0] levels, [1] batches, [2] model bytes, [3] row commits,
+                                   // [4] CSR bytes, [5] top-down levels
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the previous level's change bitmap in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
@@ -49,8 +53,8 @@ struct BfsArgs {
     unsigned long long *planes;  // [BFS_T_BITS][W] scratch: T bit planes of the batch window
     int hints;                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
                                  // 4 F_d stores evict_last, 8 F_d stores evict_first, 16 evict_normal
-    unsigned long long *lbar;    // [4] fused level-barrier counters (zeroed): arrivals and changed rows per
-                                 // level parity; nullptr: grid.sync + flag
+    unsigned long long *lbar;    // [4] counting grid-barrier counters (zeroed): arrivals [p] and changed rows
+                                 // [2 + p] by barrier-epoch parity p; nullptr: grid.sync + flag (no top-down)
     int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)
 };
 

@@ -195,7 +195,7 @@ bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const i
         unsigned long long best;
     } h;
     HM_CUDA(cudaMemcpyAsync(&h, pr.scal.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     const int P = V - 1 - (int)(h.best & 0xffffffffull);
     const int sizeP = (int)(h.best >> 32);
     const int coreP = sizeP - h.peeled;

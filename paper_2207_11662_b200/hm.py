@@ -125,10 +125,17 @@ class Context:
         return list(range(l)), [int(x) for x in dropped]
 
     def graph_info(self, g):
+        """(V, m) of graph g.  For an AND aggregate the exact m is read from the device (one host
+        round trip); hm_graph_info without the m output does not synchronise."""
         V = ctypes.c_int32()
         m = ctypes.c_int64()
         self._check(self.L.hm_graph_info(self.h, int(g), ctypes.byref(V), ctypes.byref(m), None, None))
         return V.value, m.value
+
+    def _V(self, g):
+        V = ctypes.c_int32()
+        self._check(self.L.hm_graph_info(self.h, int(g), ctypes.byref(V), None, None, None))
+        return V.value
 
     def graph_csr(self, g):
         V, m = self.graph_info(g)
@@ -157,7 +164,7 @@ class Context:
         """All-sources BFS closeness of graph g.  Returns dict of numpy arrays
         (S uint64, k int32, c float64, pen uint64) for the names in ``want``;
         with ``out`` (dict of torch CUDA tensors) writes there instead."""
-        V, _ = self.graph_info(g)
+        V = self._V(g)
         if out is None:
             res = {}
             if "S" in want:
@@ -182,7 +189,7 @@ class Context:
     def closeness_partial(self, g, shard, nshards, out=None):
         """One shard's partial distance sums S_partial[V] (uint64; numpy, or into a
         device tensor `out`): batches shard, shard + nshards, ... (hm_closeness_partial)."""
-        V, _ = self.graph_info(g)
+        V = self._V(g)
         buf = np.zeros(V, np.uint64) if out is None else out
         self._check(self.L.hm_closeness_partial(self.h, int(g), int(shard), int(nshards), _ptr(buf)))
         return buf
@@ -195,7 +202,7 @@ class Context:
 
     def closeness_results(self, g, out=None, want=("S", "k", "c", "pen")):
         """Cached closeness results of graph g (numpy by default, or into ``out``)."""
-        V, _ = self.graph_info(g)
+        V = self._V(g)
         if out is None:
             res = {}
             if "S" in want:
@@ -214,7 +221,7 @@ class Context:
 
     def cc_nodes(self, g):
         """(sorted numpy array of CC nodes, count, mean closeness)."""
-        V, _ = self.graph_info(g)
+        V = self._V(g)
         bm = np.zeros((V + 31) // 32, np.uint32)
         cnt = ctypes.c_int32()
         mu = ctypes.c_double()
@@ -223,7 +230,7 @@ class Context:
         return np.nonzero(bits)[0].astype(np.int64), cnt.value, mu.value
 
     def degrees(self, g):
-        V, _ = self.graph_info(g)
+        V = self._V(g)
         d = np.zeros(V, np.int32)
         self._check(self.L.hm_degrees(self.h, int(g), _ptr(d)))
         return d
