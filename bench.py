@@ -402,7 +402,6 @@ def run_ours(args, rank, world, local_rank):
     peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     traffic, traffic_src = measured_traffic(args)
-    nbytes_row = 8 * args.words
     per_graph = {}
     if not args.shard and not args.fused:
         ctx.sync()
@@ -420,7 +419,7 @@ def run_ours(args, rank, world, local_rank):
             sg = ctx.stats(reset=True)
             t = sg["bfs_ms"] / 1e3
             model = sg["bfs_model_bytes"]
-            comp = 2 * nbytes_row * sg["bfs_row_commits"] + sg["bfs_csr_bytes"]
+            comp = sg["bfs_state_bytes"] + sg["bfs_csr_bytes"]
             e = {"ms": sg["bfs_ms"], "levels": sg["bfs_levels"], "batches": sg["bfs_batches"],
                  "model_bytes": model, "compulsory_bytes": comp, "row_commits": sg["bfs_row_commits"],
                  "model_frac": model / t / 1e9 / peak_gbs if t > 0 else None,
@@ -712,7 +711,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--words", type=int, default=64)
+    ap.add_argument("--words", type=int, default=0, help="MS-BFS words per row (library bfs_words; 0 = automatic)")
     ap.add_argument("--hints", type=int, default=11, help="MS-BFS L2 eviction-priority bits (library bfs_hints)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",

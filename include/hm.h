@@ -60,7 +60,9 @@ void hm_destroy(hm_ctx *ctx);
 const char *hm_last_error(const hm_ctx *ctx);
 
 /* Tuning knobs (results never depend on them):
- *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16, 32 or 64; sources per batch = 64*words)
+ *   "bfs_words"   : 64-bit words per bit-parallel state row (8, 16, 32, 64 or 128; sources per batch =
+ *                   64*words; 128 only for graphs without heavy rows); 0 (default) = automatic: 128 for
+ *                   sparse graphs (average degree < 4) without heavy rows whose state exceeds 256 MB, else 64
  *   "bfs_heavy"   : degree above which a row goes to the MS-BFS heavy path (work items of 1024 arcs
  *                   claimed by whole CTAs); 0 = default: 256, or 64 on graphs of average degree < 8
  *   "bfs_blocks_per_sm" : CTAs per SM of the persistent MS-BFS kernel (1, or 0 / 2 = two)
@@ -270,6 +272,8 @@ typedef struct {
                                  8 W-byte row write: the compulsory state traffic); needs bfs_fbar = 1 */
     double bfs_csr_bytes;     /* CSR bytes of the same model: levels * (4 (rows + 1) + 4 arcs) per batch */
     int64_t bfs_td_levels;    /* levels run top-down (frontier-driven candidate rows, parameter bfs_td) */
+    double bfs_state_bytes;   /* compulsory state bytes: 2 * 8 W per row commit (own visited set read, new one
+                                 written), summed over levels and batches; needs bfs_fbar = 1 */
     int64_t host_syncs;       /* host round trips (stream synchronisations) made inside library calls: a
                                  sequence of calls with none can be captured in a CUDA graph */
 } hm_stats;

@@ -209,8 +209,9 @@ __global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32
 __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const int32_t *__restrict__ nrp, const int32_t *__restrict__ new_to_old,
                                const int32_t *__restrict__ old_to_new, int32_t *__restrict__ ncol,
-                               int32_t *heavy, int32_t *scalars, int heavy_deg, const int32_t *rem, int V) {
+                               int32_t *heavy, int32_t *scalars, const int32_t *rem, int V) {
     const int lane = threadIdx.x & 31;
+    const int heavy_deg = scalars[4];
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int n_live = scalars[0];
@@ -246,6 +247,16 @@ __global__ void k_heavy_items(const int32_t *heavy, const int32_t *nrp, const in
         }
         items[h] = n;
     }
+}
+
+// heavy-row threshold into scalars[4]: `param`, or (param <= 0, auto) 256 on graphs of average degree
+// >= 8 and 64 on sparser ones, from the exact arc count row_ptr[V] (on the device: an AND graph's
+// count is not known on the host)
+__global__ void k_heavy_threshold(const int32_t *row_ptr, int V, int param, int32_t *scalars) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    int h = param;
+    if (h <= 0) h = ((int64_t)row_ptr[V] >= (int64_t)8 * V) ? 256 : 64;
+    scalars[4] = h < BFS_MAX_LIGHT_DEG ? h : BFS_MAX_LIGHT_DEG;
 }
 
 // upper bound on the MS-BFS rows: vertices with an edge that were not peeled
@@ -389,12 +400,13 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     int64_t Vu64 = 0, nnz_u = 0;
     for (Graph *g : gs) {
         Vu64 += g->V;
-        nnz_u += g->nnz;
+        // the union CSR concatenates arcs: exact counts (an AND graph's may still be an upper bound)
+        nnz_u += gs.size() > 1 ? exact_nnz(ctx, *g) : g->nnz;
     }
     HM_REQUIRE(Vu64 < (1 << 26), HM_ERANGE, "hm_closeness supports sum V < 2^26 (packed arc format)");
     HM_REQUIRE(nnz_u < (int64_t)INT32_MAX, HM_ERANGE, "union of graphs too large for an int32 CSR");
     const int V = (int)Vu64;
-    const int W = ctx->params.bfs_words;
+    int W = ctx->params.bfs_words > 0 ? ctx->params.bfs_words : 64;   // 0 = auto (64, or 128 below)
     const unsigned gb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
     const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
     // sort keys (high << sh) | vertex with high <= V: sh = bits of V, 2 sh bits sorted
@@ -529,14 +541,15 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // heavy-row threshold: bfs_heavy, or (0, auto) 256 on graphs of average degree >= 8 and 64 on
     // sparser ones, where a row of a few dozen arcs already stalls its warp's lock-step rounds
     // (heavy sweep over C2-C4 layers and AND graphs)
-    int heavy_param = ctx->params.bfs_heavy;
-    if (heavy_param <= 0) heavy_param = (U.nnz >= (int64_t)8 * V) ? 256 : 64;
-    const int heavy_deg = heavy_param < BFS_MAX_LIGHT_DEG ? heavy_param : BFS_MAX_LIGHT_DEG;
+    const int heavy_param = ctx->params.bfs_heavy;
+    // smallest threshold the device can pick (sizes the heavy-row bound below)
+    const int heavy_min = heavy_param > 0 ? (heavy_param < BFS_MAX_LIGHT_DEG ? heavy_param : BFS_MAX_LIGHT_DEG) : 64;
+    k_heavy_threshold<<<1, 32, 0, s>>>(U.rp, V, heavy_param, scalars);
     k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
                                      n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
-                                     heavy.as<int32_t>(), scalars, heavy_deg, rem, V);
+                                     heavy.as<int32_t>(), scalars, rem, V);
     check_launch("k_relabel_cols");
-    count_launch(ctx);
+    count_launch(ctx, 2);
 
     if (ctx->params.bfs_dbg & 2) {
         if (!ctx->dbgc.p) ctx->dbgc.alloc(335872 * 8, s);
@@ -548,7 +561,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
                                 cudaMemcpyDeviceToDevice, s));
     }
     // 4. MS-BFS
-    const size_t rowb = (size_t)W * 8;
+    size_t rowb = (size_t)W * 8;
     // frontier rows only for vertices that can be BFS rows (an edge, not peeled): large sparse
     // graphs (many isolated vertices) need far less than V rows of state
     int64_t frows = V;
@@ -558,18 +571,38 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     const bool count_rows = (int64_t)V * (int64_t)rowb * 2 > ((int64_t)256 << 20);
     if (!count_rows) {
         if (frows < 32) frows = 32;                                  // as the counted path
-        const int64_t bound = U.nnz / ((int64_t)heavy_deg + 1);
+        const int64_t bound = U.nnz / ((int64_t)heavy_min + 1);
         h_heavy = (int32_t)(bound < V ? bound : V);
+        if (pr.shape_known) {
+            // the pruning round trip read the graph's shape: with no row above the heavy threshold
+            // the lean kernel runs (no heavy-row arrays), and the batch width can be chosen
+            const int hd = heavy_param > 0 ? heavy_min : (pr.arcs >= (int64_t)8 * V ? 256 : 64);
+            if (pr.maxdeg <= hd) {
+                h_heavy = 0;
+                if (ctx->params.bfs_words == 0 && pr.arcs < (int64_t)4 * pr.nonisolated && V >= 65536) {
+                    W = 128;                                         // see the counted path below
+                    rowb = (size_t)W * 8;
+                }
+            }
+        }
     } else {
         Buf cntb(16, s);
         HM_CUDA(cudaMemsetAsync(cntb.p, 0, 16, s));
         k_count_rows<<<gb, TB, 0, s>>>(U.rp, rem, V, cntb.as<int32_t>());
         check_launch("k_count_rows");
         count_launch(ctx);
-        int32_t h_rows = 0;
+        int32_t h_rows = 0, h_arcs = 0;
         HM_CUDA(cudaMemcpyAsync(&h_rows, cntb.p, 4, cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaMemcpyAsync(&h_heavy, scalars + 3, 4, cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaMemcpyAsync(&h_arcs, U.rp + V, 4, cudaMemcpyDeviceToHost, s));
         host_sync(ctx);
+        // automatic batch width (bfs_words 0): 8192 sources per batch for sparse graphs without heavy
+        // rows (average degree < 4: long, thin BFS -- the C5 AND graph 58.3 -> 50.2 ms, half the batches
+        // and level barriers), 4096 otherwise (the C5 layers: 65.3 vs 85.9 ms at 8192)
+        if (ctx->params.bfs_words == 0 && h_heavy == 0 && (int64_t)h_arcs < (int64_t)4 * h_rows && V >= 65536) {
+            W = 128;
+            rowb = (size_t)W * 8;
+        }
         frows = (int64_t)h_rows + 32;
         if (frows > V) frows = V;
         if (frows < 32) frows = 32;
@@ -587,7 +620,6 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.comp_start = cstart.as<int32_t>();
     a.scalars = scalars;
     a.heavy = heavy.as<int32_t>();
-    a.heavy_deg = heavy_deg;
     // heavy-row work items: ceil(deg / BFS_HEAVY_CHUNK) per heavy row, their prefix, and the
     // partial-row accumulators of rows with several items
     Buf hstart, hacc, hcnt;

@@ -85,7 +85,7 @@ struct Graph {
 };
 
 struct Params {
-    int bfs_words = 64;
+    int bfs_words = 0;         // 0 = auto: 64 words (4096 sources per batch), 128 for sparse graphs without heavy rows
     int bfs_heavy = 0;         // MS-BFS heavy-row degree threshold (0 = auto: 256, or 64 below average degree 8)
     int bfs_blocks_per_sm = 0;
     int bfs_chg_smem = 0;      // 1: stage the change bitmaps in shared memory each level; 0: read them via L1
@@ -180,6 +180,9 @@ void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *
 struct Prune {
     bool active = false;
     int P = -1, R = 0, peeled = 0;
+    bool shape_known = false;         // the decision round trip also read: max degree, vertices with an
+    int maxdeg = 0, nonisolated = 0;  // edge, arcs (for the host's batch-width / heavy-path choices)
+    int64_t arcs = 0;
     Buf rem, par, tsz, tD, degl, lsize, Cc, scal;   // per vertex / per component root
 };
 bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const int32_t *label, const int32_t *csize,

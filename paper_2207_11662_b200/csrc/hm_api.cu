@@ -121,8 +121,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     HM_REQUIRE(name, HM_EINVAL, "null name");
     const std::string n(name);
     if (n == "bfs_words") {
-        HM_REQUIRE(value == 8 || value == 16 || value == 32 || value == 64, HM_EINVAL,
-                   "bfs_words must be 8, 16, 32 or 64");
+        HM_REQUIRE(value == 0 || value == 8 || value == 16 || value == 32 || value == 64 || value == 128, HM_EINVAL,
+                   "bfs_words must be 0 (auto), 8, 16, 32, 64 or 128 (128: graphs without heavy rows)");
         ctx->params.bfs_words = (int)value;
     } else if (n == "bfs_heavy") {
         HM_REQUIRE(value >= 0, HM_EINVAL, "bfs_heavy must be >= 0 (0 = automatic)");
@@ -453,8 +453,8 @@ hm_status hm_sync(hm_ctx *ctx) {
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(out, HM_EINVAL, "null out");
-    unsigned long long dv[6] = {0, 0, 0, 0, 0, 0};
-    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 48, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long dv[7] = {0, 0, 0, 0, 0, 0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 56, cudaMemcpyDeviceToHost, ctx->stream));
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto &pe : ctx->pending) {
         float ms = 0.f;
@@ -474,6 +474,7 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     out->bfs_row_commits = (int64_t)dv[3];
     out->bfs_csr_bytes = (double)dv[4];
     out->bfs_td_levels = (int64_t)dv[5];
+    out->bfs_state_bytes = (double)dv[6];
     if (reset) {
         ctx->stats = Stats();
         HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));

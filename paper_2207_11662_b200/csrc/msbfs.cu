@@ -442,7 +442,7 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
 // HV: heavy-row path compiled in (false only for graphs without heavy rows: a leaner kernel)
 template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
-    constexpr int T = W / 2;           // lanes per row in the heavy path
+    constexpr int T = W / 2 < 32 ? W / 2 : 32;   // lanes per row in the heavy path (W <= 64 with heavy rows)
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
     constexpr int64_t B = 64 * W;      // sources per batch
     // light rows: TL lanes per row, VEC 16-byte chunks per lane, GD gathers in flight per lane
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     const int n_comp = a.scalars[2];
     const int n_heavy = a.scalars[3];
     const int n_items = (n_heavy > 0 && a.hstart) ? a.hstart[n_heavy] : 0;   // heavy-row items
-    const int heavy_deg = a.heavy_deg;
+    const int heavy_deg = a.scalars[4];
     int32_t *su = sm.su[wib];
     uint8_t *sr = sm.sr[wib];
     int16_t *seg = sm.seg[wib];
@@ -628,7 +628,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 
             // ---- heavy rows (heavy_items): items of BFS_HEAVY_CHUNK arcs, claimed after the light
             // units (below); HM_HEAVY_DYN 0 deals them round-robin here instead
-            if (HV && !HM_HEAVY_DYN && n_items > 0)
+            if constexpr (HV && !HM_HEAVY_DYN)
+                if (n_items > 0)
                 nchg = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                 a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
                                                 hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn,
@@ -846,7 +847,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             // heavy items claimed dynamically by the CTAs as they finish their light units (a CTA
             // holding a hub no longer finishes last; C4 layers -5 %, C3 -6 % against dealing them
             // round-robin before the light units; compiling both placements in is slower than either)
-            if (HV && HM_HEAVY_DYN && n_items > 0)
+            if constexpr (HV && HM_HEAVY_DYN)
+                if (n_items > 0)
                 nchg += heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                  a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
                                                  n_heavy, hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn,
@@ -880,7 +882,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             PROF_MARK(pf, 7);
             const int fv = sm.flag;
             if (gtid == 0) {
-                if (sm.nlast > 0) a.counters[3] += (unsigned long long)sm.nlast;   // row commits
+                if (sm.nlast > 0) {
+                    a.counters[3] += (unsigned long long)sm.nlast;                  // row commits
+                    a.counters[6] += (unsigned long long)sm.nlast * 2ull * 8ull * W;   // own read + row write
+                }
                 if (td) a.counters[5] += 1ull;                                      // top-down levels
             }
             if (a.dbgc && gtid == 0) {
@@ -913,7 +918,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s) {
     const void *kern = nullptr;
     int block = BLOCK_PLAIN;
-    if (TL == 0) TL = (W == 64) ? 16 : W / 2;
+    if (TL == 0) TL = (W >= 64) ? 16 : W / 2;
     const int vec = W / (2 * TL);
     const int minb = blocks_per_sm == 1 ? 1 : 2;
     // gathers in flight per lane: 4 at W = 64 with 2 CTAs/SM (round 2, visited-set rows: C5 layer
@@ -943,6 +948,18 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
         break;
         HM_MSBFS_CASE(64, 16, 2, 2)
+    case ((128 * 100 + 16) * 100 + 2 * 10 + 2):               // W = 128: graphs without heavy rows only
+        if (a.hstart) return -1;
+        kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false>
+                    : (const void *)msbfs_kernel<128, 16, 2, 2, false, false>;
+        block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
+        break;
+    case ((128 * 100 + 16) * 100 + 4 * 10 + 2):
+        if (a.hstart) return -1;
+        kern = a.tw ? (const void *)msbfs_kernel<128, 16, 4, 2, true, false>
+                    : (const void *)msbfs_kernel<128, 16, 4, 2, false, false>;
+        block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
+        break;
         HM_MSBFS_CASE(64, 16, 4, 1)
         HM_MSBFS_CASE(64, 16, 8, 2)
         HM_MSBFS_CASE(64, 16, 8, 1)

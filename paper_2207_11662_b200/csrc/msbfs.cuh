@@ -22,13 +22,13 @@ struct BfsArgs {
     const int2 *cinfo;           // per live row: (first row of its component, component size)
     const int32_t *comp_size;    // per component rank (descending sizes)
     const int32_t *comp_start;   // per component rank: first row
-    const int32_t *scalars;      // [0] n_live, [1] n_giant (largest size), [2] n_comp, [3] n_heavy
+    const int32_t *scalars;      // [0] n_live, [1] n_giant (largest size), [2] n_comp, [3] n_heavy,
+                                 // [4] heavy-row degree threshold
     const int32_t *heavy;        // rows with degree > heavy_deg (any order)
     const int32_t *hstart;       // [n_heavy + 1] first item of each heavy row (ceil(deg / BFS_HEAVY_CHUNK) items)
     unsigned long long *hacc;    // [n_heavy][W] zeroed: partial OR rows of multi-item heavy rows
     int32_t *hcnt;               // [n_heavy] zeroed: items of the row done this level
     int32_t *hclaim;             // [3] heavy-item claim counters, rotated by level
-    int32_t heavy_deg;
     uint64_t *F[2];              // [n_live][W] visited-set rows V(v), double-buffered: a row that
                                  // changes at level d writes V_d(v) into F[d & 1]
     uint32_t *chg[3];            // row bitmaps "changed at level", rotating over 3 levels
@@ -42,7 +42,7 @@ struct BfsArgs {
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches, [2] model bytes, [3] row commits,
-                                   // [4] CSR bytes, [5] top-down levels
+                                   // [4] CSR bytes, [5] top-down levels, [6] state bytes of the commits
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the previous level's change bitmap in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)

@@ -127,6 +127,22 @@ __global__ void k_prune_stats(const int32_t *label, const int32_t *csize, const 
     }
 }
 
+// graph shape for the host decisions taken at the same round trip: [0] max degree, [1] vertices
+// with an edge, [2] arcs
+__global__ void k_graph_stats(const int32_t *rp, int V, int32_t *out) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        const int deg = rp[v + 1] - rp[v];
+        const unsigned act = __activemask();
+        const int mx = (int)__reduce_max_sync(act, (unsigned)deg);
+        const unsigned ne = __ballot_sync(act, deg > 0);
+        if ((threadIdx.x & 31) == __ffs(act) - 1) {
+            atomicMax(out + 0, mx);
+            if (ne) atomicAdd(out + 1, __popc(ne));
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[2] = rp[V];
+}
+
 // (1) constant, then (2) top-down over the peeling rounds; S in original order
 __global__ void k_prune_finish(const int32_t *label, const int32_t *csize, const int32_t *rem, const int32_t *par,
                                const uint32_t *tsz, const unsigned long long *Cc, const int32_t *scal,
@@ -188,11 +204,14 @@ bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const i
     k_prune_stats<<<gb, TB, 0, s>>>(label, csize, rem, tsz, best, pr.lsize.as<int32_t>(),
                                    pr.Cc.as<unsigned long long>(), tD, scal + 4, V);
     check_launch("k_prune_stats");
-    count_launch(ctx, 3);
-    // one host round trip decides whether the pruned BFS pays
+    k_graph_stats<<<gb, TB, 0, s>>>(rp, V, scal + 10);
+    check_launch("k_graph_stats");
+    count_launch(ctx, 4);
+    // one host round trip decides whether the pruned BFS pays (and brings the graph's shape along)
     struct {
         int32_t R, peeled, f0, f1, lsizeP_unused, max_other, maxT, pad;
         unsigned long long best;
+        int32_t maxdeg, nonisolated, arcs, pad2;
     } h;
     HM_CUDA(cudaMemcpyAsync(&h, pr.scal.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     host_sync(ctx);
@@ -202,6 +221,10 @@ bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const i
     pr.R = h.R;
     pr.peeled = h.peeled;
     pr.P = P;
+    pr.shape_known = true;
+    pr.maxdeg = h.maxdeg;
+    pr.nonisolated = h.nonisolated;
+    pr.arcs = h.arcs;
     // worth it: >= 1 % of P peeled; P's core still the strictly largest live component
     // (so it stays the first, "giant" batch component); T fits the kernel's bit planes
     pr.active = h.peeled > 0 && (int64_t)h.peeled * 100 >= sizeP && coreP > h.max_other &&

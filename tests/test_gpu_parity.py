@@ -90,8 +90,11 @@ def test_psi_special(hm, name, V, E):
     res = O.analyze(V, E)
     # narrow batches (B = 512: several batches per component), other team widths and occupancies
     for words, team, bps, unit, prune, fbar in ((8, 0, 0, 8, 1, 1), (16, 4, 0, 16, 0, 0), (64, 32, 1, 32, 1, 0),
-                                                (64, 16, 1, 4, 0, 1), (32, 16, 1, 2, 1, 1), (64, 16, 0, 8, 1, 1)):
+                                                (64, 16, 1, 4, 0, 1), (32, 16, 1, 2, 1, 1), (64, 16, 0, 8, 1, 1),
+                                                (128, 0, 0, 0, 1, 1), (128, 0, 0, 4, 0, 0)):
         with hm() as ctx:
+            if words == 128:                     # 8192 sources per batch: no heavy rows
+                ctx.set_param("bfs_heavy", 1 << 30)
             ctx.set_param("bfs_fbar", fbar)
             ctx.set_param("bfs_prune", prune)
             ctx.set_param("bfs_words", words)
@@ -130,9 +133,9 @@ def test_tuning_invariance(hm):
     V = 3000
     E = {tuple(e) for e in random_graph(V, 6 * V, seed=77, kind="rmat").tolist()}
     res = O.analyze(V, E)
-    for words in (8, 16, 32, 64):
-        for heavy in (4, 64, 100000):
-            for bps in (0, 1):
+    for words in (8, 16, 32, 64, 128):
+        for heavy in ((4, 64, 100000) if words < 128 else (1 << 30,)):
+            for bps in ((0, 1) if words < 128 else (0,)):
                 for chg_smem, unit, inter, prune, fbar in ((0, 32, 0, 0, 1), (1, 8, 1, 1, 0), (0, 2, 1, 1, 1)):
                     with hm() as ctx:
                         ctx.set_param("bfs_fbar", fbar)
@@ -554,7 +557,7 @@ def _shape(rng, t):
 
 def test_random_sweep_all_knobs(hm):
     rng = random.Random(20220722)
-    knobs = dict(bfs_words=[8, 16, 32, 64], bfs_prune=[0, 1, 2], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
+    knobs = dict(bfs_words=[0, 8, 16, 32, 64, 128], bfs_prune=[0, 1, 2], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
                  bfs_chg_smem=[0, 1], bfs_unit=[0, 2, 4, 8, 16, 32], bfs_heavy=[0, 2, 16, 256], bfs_blocks_per_sm=[0, 1],
                  bfs_fbar=[0, 1], cc_init=[0, 1, 2], bfs_td=[0, 2, 8, 32, 1 << 20])
     with hm() as ctx:
@@ -564,6 +567,8 @@ def test_random_sweep_all_knobs(hm):
             pick = {k: rng.choice(vals) for k, vals in knobs.items()}
             # gathers in flight: every instantiated value at W = 64, 2 CTAs/SM (the bench path)
             pick["bfs_gd"] = rng.choice([0, 2, 4, 8]) if pick["bfs_words"] == 64 and pick["bfs_blocks_per_sm"] != 1 else 0
+            if pick["bfs_words"] == 128:           # 8192 sources per batch: graphs without heavy rows only
+                pick.update(bfs_heavy=1 << 30, bfs_blocks_per_sm=0, bfs_gd=rng.choice([0, 4]))
             for k, v in pick.items():
                 ctx.set_param(k, v)
             ctx.load_layers(V, [edges_arr(E)])

@@ -12,7 +12,7 @@ $P > gpurun_out/plain3.log 2>&1 && \
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none \
       -k regex:msbfs -c ${NCU_C:-4} -o gpurun_out/msbfs_traffic -f $P > gpurun_out/ncu_traffic.log 2>&1
 echo "ncu traffic rc=$?"
-python tools/ncu_traffic.py gpurun_out/msbfs_traffic.ncu-rep gpurun_out/r2_msbfs_traffic_$CFG.json $CFG 64 11 && \
+python tools/ncu_traffic.py gpurun_out/msbfs_traffic.ncu-rep gpurun_out/r2_msbfs_traffic_$CFG.json $CFG 0 11 && \
   cp gpurun_out/r2_msbfs_traffic_$CFG.json profiles/
 timeout 900 python bench.py --config $CFG ${BENCH_ARGS} > gpurun_out/bench_$CFG.log 2>&1; echo "bench rc=$?"
 tail -1 gpurun_out/bench_$CFG.log | cut -c1-600
