@@ -22,3 +22,13 @@ CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e
 $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "ncu list rc=$?"
+# full ncu capture of the 4 MS-BFS launches of bench.py's setup pass (3 layers + AND of one HoMLN)
+[ -n "$NO_FULL" ] && exit 0
+P="python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-graph"
+$P > gpurun_out/plain2.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:msbfs -c ${NCU_C:-4} -o gpurun_out/msbfs_full_$CFG -f $P > gpurun_out/ncu_full.log 2>&1
+echo "ncu full rc=$?"
+for k in 0 3; do python tools/ncu_summary.py gpurun_out/msbfs_full_$CFG.ncu-rep $k > gpurun_out/ncu_summary_${CFG}_$k.txt 2>&1; done
+python tools/launch_summary.py gpurun_out/launches_$CFG.csv > gpurun_out/launch_summary_$CFG.txt 2>&1
+# source-batch sharding at N = 1 (the partial/combine split's own cost)
+timeout 900 python bench.py --config $CFG --shard --no-cpu-baseline --no-e2e > gpurun_out/bench_shard_$CFG.log 2>&1; echo "shard rc=$?"
