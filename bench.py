@@ -167,6 +167,9 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_param("bfs_words", args.words)
     ctx.set_param("bfs_hints", args.hints)
     ctx.set_param("timing", 1)
+    for kv in args.set:                      # extra library parameters (A/B experiments)
+        k, v = kv.split("=")
+        ctx.set_param(k, int(v))
     host_layers = [torch.from_numpy(L).pin_memory() for L in h.layers]
     dev_layers = [t.to(f"cuda:{dev}") for t in host_layers]
     torch.cuda.synchronize()
@@ -724,6 +727,7 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo: host-staged, for the 2-rank test on one GPU)")
     ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (tests only)")
+    ap.add_argument("--set", action="append", default=[], help="name=value library parameter (experiments)")
     ap.add_argument("--V", type=int, default=None, help="scale the config to V vertices (tests only)")
     ap.add_argument("--dump", default=None,
                     help="after the run, rank 0 writes every graph's closeness results and every ranked list "
