@@ -579,7 +579,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
             const int hd = heavy_param > 0 ? heavy_min : (pr.arcs >= (int64_t)8 * V ? 256 : 64);
             if (pr.maxdeg <= hd) {
                 h_heavy = 0;
-                if (ctx->params.bfs_words == 0 && pr.arcs < (int64_t)4 * pr.nonisolated && V >= 65536) {
+                if (ctx->params.bfs_words == 0 && ctx->params.bfs_team == 0 && ctx->params.bfs_gd == 0 &&
+                    ctx->params.bfs_blocks_per_sm != 1 && pr.arcs < (int64_t)4 * pr.nonisolated && V >= 65536) {
                     W = 128;                                         // see the counted path below
                     rowb = (size_t)W * 8;
                 }
@@ -599,7 +600,9 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         // automatic batch width (bfs_words 0): 8192 sources per batch for sparse graphs without heavy
         // rows (average degree < 4: long, thin BFS -- the C5 AND graph 58.3 -> 50.2 ms, half the batches
         // and level barriers), 4096 otherwise (the C5 layers: 65.3 vs 85.9 ms at 8192)
-        if (ctx->params.bfs_words == 0 && h_heavy == 0 && (int64_t)h_arcs < (int64_t)4 * h_rows && V >= 65536) {
+        if (ctx->params.bfs_words == 0 && ctx->params.bfs_team == 0 && ctx->params.bfs_gd == 0 &&
+            ctx->params.bfs_blocks_per_sm != 1 && h_heavy == 0 && (int64_t)h_arcs < (int64_t)4 * h_rows &&
+            V >= 65536) {
             W = 128;
             rowb = (size_t)W * 8;
         }

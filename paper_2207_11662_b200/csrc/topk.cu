@@ -189,14 +189,16 @@ __device__ __forceinline__ bool less_kv(uint64_t ka, uint32_t ia, uint64_t kb, u
 }
 
 // one block, K <= SORT_MAX: bitonic sort of (key, id) then write ids
-__global__ void __launch_bounds__(1024) k_sort_small(const uint64_t *ok, const uint32_t *oid, int K, int P,
+// sort the first n (key, id) pairs (ids = positions when oid is null) in shared memory and write
+// the first K ids; P = the power of two >= n
+__global__ void __launch_bounds__(1024) k_sort_small(const uint64_t *ok, const uint32_t *oid, int n, int K, int P,
                                                      int32_t *out) {
     extern __shared__ unsigned char smem[];
     uint64_t *sk = reinterpret_cast<uint64_t *>(smem);
     uint32_t *si = reinterpret_cast<uint32_t *>(sk + P);
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        sk[i] = i < K ? ok[i] : ~0ull;
-        si[i] = i < K ? oid[i] : 0xffffffffu;
+        sk[i] = i < n ? ok[i] : ~0ull;
+        si[i] = i < n ? (oid ? oid[i] : (uint32_t)i) : 0xffffffffu;
     }
     __syncthreads();
     for (int size = 2; size <= P; size <<= 1) {
@@ -256,6 +258,16 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
         count_launch(ctx, 10);
         return;
     }
+    if (n <= SORT_MAX) {
+        // small inputs: one CTA sorts all n (key, id) pairs in shared memory (one launch instead of
+        // the select pipeline; C1: 4 top-K lists per step)
+        int P = 1;
+        while (P < n) P <<= 1;
+        k_sort_small<<<1, 1024, (size_t)P * 12, s>>>(d_keys, nullptr, n, K, P, d_ids_out);
+        check_launch("topk small");
+        count_launch(ctx, 1);
+        return;
+    }
     Buf stb(sizeof(SelState), s), ok((size_t)K * 8, s), oid((size_t)K * 4, s);
     SelState *st = stb.as<SelState>();
     HM_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), s));
@@ -287,7 +299,7 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
     const size_t sm = (size_t)P * 12;
     if (sm > 48 * 1024)
         HM_CUDA(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_sort_small<<<1, 1024, sm, s>>>(ok.as<uint64_t>(), oid.as<uint32_t>(), K, P, d_ids_out);
+    k_sort_small<<<1, 1024, sm, s>>>(ok.as<uint64_t>(), oid.as<uint32_t>(), K, K, P, d_ids_out);
     check_launch("topk");
     count_launch(ctx, 1);
 }
