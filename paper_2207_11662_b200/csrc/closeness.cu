@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "msbfs.cuh"
+#include "exactsum.cuh"
 
 namespace hm {
 namespace {
@@ -342,6 +343,248 @@ __global__ void k_cc_bitmap(const double *c, const double *mu, uint32_t *bm, int
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Small graphs (V <= SMALL_V, one graph, no pruning): the whole pre-processing (components,
+// component order, relabelling, packed CSR, heavy list) and the whole post-processing (finalize,
+// exact mean, CC-node bitmap) each run in ONE CTA out of shared memory, instead of ~30 grid-wide
+// launches that a 1000-vertex graph cannot fill (C1: the step is launch-bound).
+constexpr int SMALL_V = 4096;
+constexpr int SMALL_T = 1024;
+
+__device__ __forceinline__ int s_find(int *p, int x) {
+    while (true) {
+        const int px = p[x];
+        if (px == x) return x;
+        const int ppx = p[px];
+        if (ppx != px) p[x] = ppx;     // path halving: ppx is an ancestor of x
+        x = px;
+    }
+}
+
+// in-place exclusive scan of a[0..n) by one CTA of SMALL_T threads; returns the total
+__device__ int s_excl_scan(int *a, int n, int *ws) {
+    const int per = (n + SMALL_T - 1) / SMALL_T;
+    const int b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+    int sum = 0;
+    for (int i = b0; i < b1; ++i) sum += a[i];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int w = ws[lane];                       // SMALL_T / 32 == 32 warps
+        int wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        ws[lane] = wi - w;
+        if (lane == 31) ws[32] = wi;
+    }
+    __syncthreads();
+    int run = ws[wid] + incl - sum;
+    for (int i = b0; i < b1; ++i) {
+        const int x = a[i];
+        a[i] = run;
+        run += x;
+    }
+    const int total = ws[32];
+    __syncthreads();
+    return total;
+}
+
+// ascending bitonic sort of P (a power of two) 64-bit keys in shared memory
+__device__ void s_bitonic(uint64_t *k, int P) {
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += SMALL_T) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const uint64_t a = k[i], b = k[j];
+                    if (up ? (a > b) : (a < b)) {
+                        k[i] = b;
+                        k[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// Same outputs as steps 1-3 of closeness_multi (no pruning): label / csize by root id, the
+// component table (size_s, cstart), n2o / o2n, cinfo, the relabelled packed CSR, the heavy list
+// and scalars [0] n_live [1] n_giant [2] n_comp [3] n_heavy [4] heavy threshold.
+__global__ void __launch_bounds__(SMALL_T) k_small_prep(const int32_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                                        int V, int P, int sh, int heavy_param, int32_t *label,
+                                                        int32_t *csize, int32_t *size_s, int32_t *cstart,
+                                                        int32_t *n2o, int32_t *o2n, int32_t *nrp, int2 *cinfo,
+                                                        int32_t *ncol, int32_t *heavy, int32_t *scalars) {
+    extern __shared__ unsigned long long s_mem[];
+    uint64_t *key = reinterpret_cast<uint64_t *>(s_mem);             // [P]
+    int *par = reinterpret_cast<int *>(key + P);                       // [V] parent, then label
+    int *lab = par + V;                                                // [V] label
+    int *csz = lab + V;                                                // [V] size by root id
+    int *aux = csz + V;                                                // [V + 1] rank of root / degrees
+    int *ssz = aux + V + 1;                                            // [V + 1] size by rank, then cstart
+    int *ws = ssz + V + 1;                                             // [33] scan scratch
+    __shared__ int s_ncomp, s_nlive;
+    const uint64_t lo = (1ull << sh) - 1ull;
+    for (int v = threadIdx.x; v < V; v += SMALL_T) {
+        par[v] = v;
+        csz[v] = 0;
+    }
+    if (threadIdx.x == 0) {
+        s_ncomp = 0;
+        s_nlive = 0;
+    }
+    __syncthreads();
+    // 1. components: lock-free union in shared memory (larger root under smaller)
+    for (int u = threadIdx.x; u < V; u += SMALL_T)
+        for (int j = rp[u]; j < rp[u + 1]; ++j) {
+            const int w = col[j];
+            if (w <= u) continue;
+            int ru = s_find(par, u), rw = s_find(par, w);
+            while (ru != rw) {
+                if (ru < rw) { const int t = ru; ru = rw; rw = t; }
+                const int old = atomicCAS(par + ru, ru, rw);
+                if (old == ru) break;
+                ru = s_find(par, old);
+                rw = s_find(par, rw);
+            }
+        }
+    __syncthreads();
+    for (int v = threadIdx.x; v < V; v += SMALL_T) lab[v] = s_find(par, v);
+    __syncthreads();
+    for (int v = threadIdx.x; v < V; v += SMALL_T) {
+        atomicAdd(csz + lab[v], 1);
+        label[v] = lab[v];
+    }
+    __syncthreads();
+    // 2. component order: (size desc, root asc); non-roots sort last
+    for (int i = threadIdx.x; i < P; i += SMALL_T)
+        key[i] = i < V ? ((lab[i] == i) ? (((uint64_t)(V - csz[i]) << sh) | (uint64_t)i) : ((uint64_t)V << sh))
+                       : ~0ull;
+    __syncthreads();
+    s_bitonic(key, P);
+    for (int i = threadIdx.x; i < V; i += SMALL_T) {
+        csize[i] = csz[i];
+        const uint64_t k = key[i];
+        if ((k >> sh) < (uint64_t)V) {
+            ssz[i] = V - (int)(k >> sh);
+            aux[(int)(k & lo)] = i;                                     // rank of the root
+            if (i + 1 == V || (key[i + 1] >> sh) >= (uint64_t)V) s_ncomp = i + 1;
+        } else {
+            ssz[i] = 0;
+        }
+    }
+    __syncthreads();
+    const int n_comp = s_ncomp;
+    for (int i = threadIdx.x; i < V; i += SMALL_T) size_s[i] = ssz[i];
+    __syncthreads();
+    s_excl_scan(ssz, V, ws);                                            // ssz := cstart
+    for (int i = threadIdx.x; i < n_comp; i += SMALL_T) {
+        const int sz = size_s[i];
+        if (sz > 1 && (i + 1 == n_comp || size_s[i + 1] <= 1)) s_nlive = ssz[i] + sz;
+    }
+    for (int i = threadIdx.x; i < V; i += SMALL_T) cstart[i] = ssz[i];
+    __syncthreads();
+    // vertex order: (component rank, id)
+    for (int i = threadIdx.x; i < P; i += SMALL_T)
+        key[i] = i < V ? (((uint64_t)aux[lab[i]] << sh) | (uint64_t)i) : ~0ull;
+    __syncthreads();
+    s_bitonic(key, P);
+    for (int i = threadIdx.x; i < V; i += SMALL_T) {
+        const int old = (int)(key[i] & lo);
+        const int r = (int)(key[i] >> sh);
+        n2o[i] = old;
+        o2n[old] = i;
+        aux[i] = rp[old + 1] - rp[old];                                 // new degree
+        cinfo[i] = make_int2(ssz[r], size_s[r]);
+    }
+    if (threadIdx.x == 0) aux[V] = 0;
+    __syncthreads();
+    const int nnz = s_excl_scan(aux, V + 1, ws);                        // aux := relabelled row_ptr
+    for (int i = threadIdx.x; i <= V; i += SMALL_T) nrp[i] = aux[i];
+    int hd = heavy_param;
+    if (hd <= 0) hd = ((int64_t)nnz >= (int64_t)8 * V) ? 256 : 64;
+    if (hd > BFS_MAX_LIGHT_DEG) hd = BFS_MAX_LIGHT_DEG;
+    __syncthreads();
+    // 3. packed arcs (relabelled neighbour << 5 | row & 31), heavy rows
+    const int n_live = s_nlive;
+    for (int i = threadIdx.x; i < n_live; i += SMALL_T) {
+        const int old = (int)(key[i] & lo);
+        const int rb = rp[old], re = rp[old + 1], ob = aux[i];
+        for (int j = rb; j < re; ++j) ncol[ob + (j - rb)] = (o2n[col[j]] << 5) | (i & 31);
+        if (re - rb > hd) heavy[atomicAdd(scalars + 3, 1)] = i;
+    }
+    if (threadIdx.x == 0) {
+        scalars[0] = n_live;
+        scalars[1] = size_s[0] > 1 ? size_s[0] : 0;
+        scalars[2] = n_comp;
+        scalars[4] = hd;
+    }
+}
+
+// finalize (S, k, WF closeness, n-penalty sum, degree), exact mean and CH bitmap in one CTA
+__global__ void __launch_bounds__(SMALL_T) k_small_finish(const int32_t *o2n, const int32_t *label,
+                                                          const int32_t *csize, const int32_t *row_ptr,
+                                                          const uint64_t *S_rel, const int32_t *scalars,
+                                                          uint64_t *S, int32_t *kk, double *c, uint64_t *pen,
+                                                          int32_t *deg, uint32_t *bm, double *mu_out,
+                                                          int32_t *cnt_out, int V) {
+    __shared__ unsigned s16[2 * EXACT_NLIMB];
+    __shared__ unsigned long long acc[EXACT_NLIMB];
+    __shared__ double s_mu;
+    __shared__ int s_cnt;
+    for (int i = threadIdx.x; i < 2 * EXACT_NLIMB; i += SMALL_T) s16[i] = 0u;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int n_live = scalars[0];
+    for (int v = threadIdx.x; v < V; v += SMALL_T) {
+        const int i = o2n[v];
+        const uint64_t sv = i < n_live ? S_rel[i] : 0ull;
+        const int k = csize[label[v]];
+        double cv = 0.0;                 // Wasserman-Faust, the NetworkX order
+        if (sv > 0ull && V > 1) {
+            const double t1 = __ddiv_rn((double)(k - 1), (double)sv);
+            const double t2 = __ddiv_rn((double)(k - 1), (double)(V - 1));
+            cv = __dmul_rn(t1, t2);
+        }
+        S[v] = sv;
+        kk[v] = k;
+        c[v] = cv;
+        pen[v] = sv + (uint64_t)(V - k) * (uint64_t)V;      // n-penalty sum
+        deg[v] = row_ptr[v + 1] - row_ptr[v];
+        exact_add16(s16, cv);                                 // V <= SMALL_V < 2^16 values: exact
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < EXACT_NLIMB; i += SMALL_T) acc[i] = exact_limb16(s16, i);
+    __syncthreads();
+    if (threadIdx.x == 0) s_mu = __ddiv_rn(exact_round(acc), (double)V);   // mu = RN(sum c) / V (Z6)
+    __syncthreads();
+    const double m = s_mu;
+    const int lane = threadIdx.x & 31;
+    for (int vb = threadIdx.x & ~31; vb < V; vb += SMALL_T) {              // CH = {v : c(v) > mu}
+        const int v = vb + lane;
+        const bool in = v < V && c[v] > m;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) {
+            bm[vb >> 5] = b;
+            if (b) atomicAdd(&s_cnt, __popc(b));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *mu_out = m;
+        *cnt_out = s_cnt;
+    }
+}
+
 inline int nbits(uint64_t x) {
     int b = 0;
     while (x) { ++b; x >>= 1; }
@@ -455,6 +698,12 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         const int32_t *rp, *col;
     } U{V, nnz_u, rp_u, col_u};
 
+    // pruning: on (1), off (0), or (2, default) on from V = 4096, below which its kernels and host
+    // round trip cost more than the BFS they save (C1: 0.32 vs 0.26 ms per closeness call)
+    const bool want_prune = ctx->params.bfs_prune == 1 || (ctx->params.bfs_prune == 2 && V >= 4096);
+    // small graphs: one-CTA pre- and post-processing (k_small_prep / k_small_finish)
+    const bool small = gs.size() == 1 && !d_S_partial && !d_S_total && V <= SMALL_V && !want_prune;
+
     Buf parent((size_t)V * 4, s), label((size_t)V * 4, s), csize((size_t)V * 4, s);
     Buf key1((size_t)V * 8, s), key2((size_t)V * 8, s);
     Buf size_s((size_t)V * 4, s), cstart((size_t)V * 4, s), rank((size_t)V * 4, s);
@@ -466,6 +715,23 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     HM_CUDA(cudaMemsetAsync(scal.p, 0, 64, s));
     HM_CUDA(cudaMemsetAsync(csize.p, 0, csize.bytes, s));
 
+    Prune pr;
+    const int32_t *rem = nullptr;
+    const int heavy_param = ctx->params.bfs_heavy;
+    // smallest threshold the device can pick (sizes the heavy-row bound below)
+    const int heavy_min = heavy_param > 0 ? (heavy_param < BFS_MAX_LIGHT_DEG ? heavy_param : BFS_MAX_LIGHT_DEG) : 64;
+    if (small) {
+        int P = 1;
+        while (P < V) P <<= 1;
+        const size_t smem = (size_t)P * 8 + ((size_t)5 * V + 35) * 4;
+        HM_CUDA(cudaFuncSetAttribute(k_small_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_small_prep<<<1, SMALL_T, smem, s>>>(U.rp, U.col, V, P, sh, heavy_param, label.as<int32_t>(),
+                                              csize.as<int32_t>(), size_s.as<int32_t>(), cstart.as<int32_t>(),
+                                              n2o.as<int32_t>(), o2n.as<int32_t>(), nrp.as<int32_t>(),
+                                              cinfo.as<int2>(), ncol.as<int32_t>(), heavy.as<int32_t>(), scalars);
+        check_launch("k_small_prep");
+        count_launch(ctx);
+    } else {
     // 1. connected components
     if (ctx->params.cc_init == 1) k_cc_init<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
     else k_iota<<<gb, TB, 0, s>>>(parent.as<int32_t>(), V);
@@ -486,13 +752,9 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     count_launch(ctx, 3);
 
     // 1b. exact 2-core pruning of the largest component (prune.cu; single graph only)
-    Prune pr;
-    // pruning: on (1), off (0), or (2, default) on from V = 4096, below which its kernels and host
-    // round trip cost more than the BFS they save (C1: 0.32 vs 0.26 ms per closeness call)
-    const bool want_prune = ctx->params.bfs_prune == 1 || (ctx->params.bfs_prune == 2 && V >= 4096);
     if (want_prune && gs.size() == 1)
         prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr);
-    const int32_t *rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
+    rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
 
     if (d_S_total) {
         Graph &G = *gs[0];
@@ -541,9 +803,6 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // heavy-row threshold: bfs_heavy, or (0, auto) 256 on graphs of average degree >= 8 and 64 on
     // sparser ones, where a row of a few dozen arcs already stalls its warp's lock-step rounds
     // (heavy sweep over C2-C4 layers and AND graphs)
-    const int heavy_param = ctx->params.bfs_heavy;
-    // smallest threshold the device can pick (sizes the heavy-row bound below)
-    const int heavy_min = heavy_param > 0 ? (heavy_param < BFS_MAX_LIGHT_DEG ? heavy_param : BFS_MAX_LIGHT_DEG) : 64;
     k_heavy_threshold<<<1, 32, 0, s>>>(U.rp, V, heavy_param, scalars);
     k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
                                      n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
@@ -560,6 +819,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + (139264 + 2 * 65536) * 8, key2.p, nn * 8,
                                 cudaMemcpyDeviceToDevice, s));
     }
+    }   // !small
+
     // 4. MS-BFS
     size_t rowb = (size_t)W * 8;
     // frontier rows only for vertices that can be BFS rows (an edge, not peeled): large sparse
@@ -715,7 +976,10 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cudaEventCreate(&e1));
         HM_CUDA(cudaEventRecord(e0, s));
     }
-    const int grid = launch_msbfs(W, ctx->params.bfs_team, ctx->params.bfs_gd, a, ctx->num_sms, ctx->params.bfs_blocks_per_sm, s);
+    // small graphs: no more CTAs than one light unit per warp (cheaper level barriers)
+    const int64_t units = small ? ((frows + 31) / 32) << a.unit_shift : 0;
+    const int grid = launch_msbfs(W, ctx->params.bfs_team, ctx->params.bfs_gd, a, ctx->num_sms,
+                                  ctx->params.bfs_blocks_per_sm, s, units);
     if (grid == -1)                     // no instantiation for this (words, team, gathers, CTAs/SM)
         throw Error(HM_EINVAL, "no MS-BFS kernel for bfs_words=" + std::to_string(W) + " bfs_team=" +
                                    std::to_string(ctx->params.bfs_team) + " bfs_gd=" + std::to_string(ctx->params.bfs_gd) +
@@ -733,6 +997,20 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     count_launch(ctx);
     ctx->stats.bfs_launches += 1;
 
+    if (small) {
+        Graph &G = *gs[0];
+        const size_t nbw = (size_t)(V + 31) / 32;
+        double *d_mu = reinterpret_cast<double *>(G.ch.as<char>() + ((nbw * 4 + 7) / 8) * 8);
+        k_small_finish<<<1, SMALL_T, 0, s>>>(o2n.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(),
+                                            G.row_ptr.as<int32_t>(), Srel.as<uint64_t>(), scalars,
+                                            G.S.as<uint64_t>(), G.k.as<int32_t>(), G.c.as<double>(),
+                                            G.pen.as<uint64_t>(), G.deg.as<int32_t>(), G.ch.as<uint32_t>(), d_mu,
+                                            reinterpret_cast<int32_t *>(d_mu + 1), V);
+        check_launch("k_small_finish");
+        count_launch(ctx);
+        G.has_results = true;
+        return;
+    }
     if (d_S_partial) {
         k_partial_sums<<<grid_for(V, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(o2n.as<int32_t>(), Srel.as<uint64_t>(),
                                                                                  scalars, d_S_partial, V);

@@ -17,12 +17,12 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "exactsum.cuh"
 
 namespace hm {
 namespace {
 
-constexpr int LO = -1088;
-constexpr int NLIMB = 70;     // covers 2^-1088 .. 2^1152
+constexpr int NLIMB = EXACT_NLIMB;
 constexpr int BLOCK = 256;
 
 __global__ void __launch_bounds__(BLOCK) k_exact_accum(const double *__restrict__ x, int64_t n,
@@ -30,9 +30,9 @@ __global__ void __launch_bounds__(BLOCK) k_exact_accum(const double *__restrict_
                                                        unsigned long long *acc,
                                                        unsigned long long *count,
                                                        int32_t *bad) {
-    __shared__ unsigned long long s[NLIMB];
+    __shared__ unsigned s16[2 * NLIMB];
     __shared__ unsigned long long s_cnt;
-    for (int i = threadIdx.x; i < NLIMB; i += BLOCK) s[i] = 0ull;
+    for (int i = threadIdx.x; i < 2 * NLIMB; i += BLOCK) s16[i] = 0u;
     if (threadIdx.x == 0) s_cnt = 0ull;
     __syncthreads();
     unsigned long long my_cnt = 0;
@@ -41,36 +41,20 @@ __global__ void __launch_bounds__(BLOCK) k_exact_accum(const double *__restrict_
         const double v = x[i];
         ++my_cnt;
         const uint64_t bits = (uint64_t)__double_as_longlong(v);
-        const int ef = (int)((bits >> 52) & 0x7ff);
-        if ((bits >> 63) || ef == 0x7ff) {   // negative, inf or nan: outside the contract
+        if ((bits >> 63) || ((bits >> 52) & 0x7ff) == 0x7ff) {   // negative, inf or nan: outside the contract
             *bad = 1;
             continue;
         }
-        uint64_t m = bits & ((1ull << 52) - 1);
-        int e;
-        if (ef == 0) {
-            e = -1074;
-        } else {
-            m |= (1ull << 52);
-            e = ef - 1075;
-        }
-        if (m == 0) continue;
-        const int pos = e - LO;               // >= 14
-        const int li = pos >> 5, off = pos & 31;
-        const unsigned __int128 t = (unsigned __int128)m << off;
-        const uint64_t l0 = (uint64_t)t & 0xffffffffull;
-        const uint64_t l1 = (uint64_t)(t >> 32) & 0xffffffffull;
-        const uint64_t l2 = (uint64_t)(t >> 64) & 0xffffffffull;
-        if (l0) atomicAdd(&s[li], (unsigned long long)l0);
-        if (l1) atomicAdd(&s[li + 1], (unsigned long long)l1);
-        if (l2) atomicAdd(&s[li + 2], (unsigned long long)l2);
+        exact_add16(s16, v);
     }
     // count: warp reduce then shared atomic
     for (int o = 16; o > 0; o >>= 1) my_cnt += __shfl_xor_sync(0xffffffffu, my_cnt, o);
     if ((threadIdx.x & 31) == 0 && my_cnt) atomicAdd(&s_cnt, my_cnt);
     __syncthreads();
-    for (int i = threadIdx.x; i < NLIMB; i += BLOCK)
-        if (s[i]) atomicAdd(&acc[i], s[i]);
+    for (int i = threadIdx.x; i < NLIMB; i += BLOCK) {
+        const unsigned long long x = exact_limb16(s16, i);
+        if (x) atomicAdd(&acc[i], x);
+    }
     if (threadIdx.x == 0 && s_cnt) atomicAdd(count, s_cnt);
 }
 
@@ -79,36 +63,7 @@ __global__ void k_exact_finish(const unsigned long long *acc_in, const unsigned 
                                double *mean_out, int32_t *count_out, const int32_t *bad, int32_t *bad_out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (bad_out) *bad_out = *bad;
-    uint32_t L[NLIMB + 2];
-    unsigned long long carry = 0;
-    for (int i = 0; i < NLIMB; ++i) {
-        const unsigned long long v = acc_in[i] + carry;   // < 2^64 (acc < 2^63, carry < 2^32)
-        L[i] = (uint32_t)(v & 0xffffffffull);
-        carry = v >> 32;
-    }
-    L[NLIMB] = (uint32_t)(carry & 0xffffffffull);
-    L[NLIMB + 1] = (uint32_t)(carry >> 32);
-    int t = NLIMB + 1;
-    while (t >= 0 && L[t] == 0) --t;
-    double sum = 0.0;
-    if (t >= 0) {
-        const uint32_t hi = L[t];
-        const uint32_t mid = t >= 1 ? L[t - 1] : 0u;
-        const uint32_t lo = t >= 2 ? L[t - 2] : 0u;
-        bool sticky = false;
-        for (int i = t - 3; i >= 0; --i)
-            if (L[i]) { sticky = true; break; }
-        const unsigned __int128 X = ((unsigned __int128)hi << 64) | ((unsigned __int128)mid << 32) | lo;
-        const int p = 64 + (31 - __clz((int)hi));           // index of X's top bit
-        const int shift = p - 52;                             // >= 12
-        uint64_t q = (uint64_t)(X >> shift);
-        const unsigned __int128 rem = X & ((((unsigned __int128)1) << shift) - 1);
-        const unsigned __int128 half = ((unsigned __int128)1) << (shift - 1);
-        if (rem > half || (rem == half && (sticky || (q & 1ull)))) ++q;
-        // value = q * 2^(shift + 32 (t-2) + LO); q <= 2^53 is exact in binary64
-        const int e2 = shift + 32 * (t - 2) + LO;
-        sum = ldexp((double)q, e2);
-    }
+    const double sum = exact_round(acc_in);
     const unsigned long long n = *count;
     if (count_out) *count_out = (int32_t)n;
     *mean_out = n ? __ddiv_rn(sum, (double)n) : 0.0;
@@ -125,7 +80,11 @@ void exact_mean(hm_ctx *ctx, const double *d_x, int64_t n, const uint8_t *d_mask
     unsigned long long *d_cnt = d_acc + NLIMB;
     int32_t *d_bad = reinterpret_cast<int32_t *>(d_acc + NLIMB + 1);
     if (n > 0) {
-        k_exact_accum<<<grid_for(n, BLOCK, (int64_t)ctx->num_sms * 8), BLOCK, 0, s>>>(
+        // blocks: at most EXACT_MAX_PER_BLOCK values each (the 16-bit-half counters stay exact)
+        int64_t nb = grid_for(n, BLOCK, (int64_t)ctx->num_sms * 8);
+        const int64_t need = (n + EXACT_MAX_PER_BLOCK - 1) / EXACT_MAX_PER_BLOCK;
+        if (nb < need) nb = need;
+        k_exact_accum<<<(unsigned)nb, BLOCK, 0, s>>>(
             d_x, n, d_mask_or_null, d_acc, d_cnt, d_bad);
         check_launch("k_exact_accum");
         count_launch(ctx);

@@ -915,7 +915,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 
 }  // namespace
 
-int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s) {
+int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s,
+                 int64_t units) {
     const void *kern = nullptr;
     int block = BLOCK_PLAIN;
     if (TL == 0) TL = (W >= 64) ? 16 : W / 2;
@@ -973,7 +974,11 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, block, dyn) != cudaSuccess) return -2;
     if (maxb < 1) return -3;
     const int b = (minb < maxb) ? minb : maxb;
-    const int grid = num_sms * b;
+    int grid = num_sms * b;
+    if (units > 0) {
+        const int64_t need = (units + block / 32 - 1) / (block / 32);
+        if (need < grid) grid = need < 1 ? 1 : (int)need;
+    }
     BfsArgs args = a;
     void *kargs[] = {(void *)&args};
     if (cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(block), kargs, dyn, s) != cudaSuccess) return -4;

@@ -63,6 +63,9 @@ struct BfsArgs {
 // TL = lanes per state row in the light path (0 = default: W/2, 16 at W = 64);
 // GD = gathers in flight per lane (0 = default for the occupancy);
 // blocks_per_sm == 1 selects the 1-CTA/SM (128-register) instantiations, else 2 CTAs/SM.
-int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s);
+// units > 0: the light-path work units of the largest batch; the grid is capped at one unit per warp
+// (small graphs: fewer CTAs in every level barrier).
+int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int blocks_per_sm, cudaStream_t s,
+                 int64_t units = 0);
 
 }  // namespace hm
