@@ -75,9 +75,11 @@ const char *hm_last_error(const hm_ctx *ctx);
  *              flag; 1 (default) one counter atomic per CTA carries both (arrival and "row changed")
  *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
- *   "cc_init"     : connected components: 2 (default) sampled union-find (unite each vertex with its
- *                   first 2 neighbours, then only rows outside the most frequent root unite over the
- *                   rest); 0 union over every arc; 1 as 0 starting from parent = smallest neighbour
+ *   "cc_init"     : connected components: 3 (default) min-label hooking (atomicMin of the larger root
+ *                   under the smaller) and pointer jumping, rounds until no hook changes, in one
+ *                   cooperative launch; 2 sampled union-find (unite each vertex with its first 2
+ *                   neighbours, then only rows outside the most frequent root unite over the rest);
+ *                   0 union over every arc; 1 as 0 starting from parent = smallest neighbour
  *   "bfs_unit"    : rows per MS-BFS light-path work unit (32, 16, 8, 4 or 2; 0 = default: chosen from
  *                   the live rows per warp of the grid, 32 on C5-sized graphs)
  *   "bfs_team"    : lanes per state row in the MS-BFS light path (0 = default, 4, 8, 16, 32; <= words/2)
@@ -86,7 +88,8 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   then only candidate rows pull -- when frontier rows * bfs_td <= the batch's rows, else
  *                   bottom-up over every row not yet complete; 0 = always bottom-up
  *   "bfs_chg_smem": 1 stages the per-level change bitmaps in shared memory, 0 (default) reads them via L1
- *   "timing"      : 1 = record CUDA events around the MS-BFS kernel (see hm_get_stats)
+ *   "timing"      : 1 = record CUDA events around the MS-BFS kernel, 2 = also around every phase of
+ *                   closeness / compose / top-K / aggregation (see hm_get_stats)
  *   "bfs_dbg"     : debug: bit 1 (value 2) = per-level counters and times (hm_debug_counts);
  *                   bits 8.. = the one level to profile in HM_MSBFS_PROF builds
  * Unknown name -> HM_EINVAL. */
@@ -276,6 +279,9 @@ typedef struct {
                                  written), summed over levels and batches; needs bfs_fbar = 1 */
     int64_t host_syncs;       /* host round trips (stream synchronisations) made inside library calls: a
                                  sequence of calls with none can be captured in a CUDA graph */
+    double phase_ms[10];      /* with timing = 2: CUDA-event time per phase -- [0] components, [1] pruning
+                                 decision, [2] relabel, [3] MS-BFS setup, [4] MS-BFS, [5] finalize + mean +
+                                 CC nodes, [6] compose, [7] top-K, [8] aggregation, [9] other */
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
 

@@ -24,7 +24,8 @@ class HmStats(ctypes.Structure):
                 ("bfs_levels", ctypes.c_int64), ("bfs_batches", ctypes.c_int64),
                 ("bfs_model_bytes", ctypes.c_double), ("bfs_row_commits", ctypes.c_int64),
                 ("bfs_csr_bytes", ctypes.c_double), ("bfs_td_levels", ctypes.c_int64),
-                ("bfs_state_bytes", ctypes.c_double), ("host_syncs", ctypes.c_int64)]
+                ("bfs_state_bytes", ctypes.c_double), ("host_syncs", ctypes.c_int64),
+                ("phase_ms", ctypes.c_double * 10)]
 
 
 # name -> (restype, argtypes); must match include/hm.h (tests/test_abi.py checks the names)

@@ -11,6 +11,7 @@
 //      sum, degree;
 //   6. mu = RN(exact sum c) / V (exactsum.cu) and CH = {v : c(v) > mu}.
 #include <cmath>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -127,6 +128,72 @@ __global__ void k_cc_union(const int32_t *__restrict__ row_ptr, const int32_t *_
                 rv = cc_find(p, rv);
             }
         }
+    }
+}
+
+// Components by min-label hooking and pointer jumping (Shiloach-Vishkin style), in one cooperative
+// launch (cc_init 3, default).  f[v] <= v always holds (every update is an atomicMin to a vertex of
+// the same component), so f is a forest whose roots are the smallest ids.  Per round: every edge
+// hooks the larger of its endpoints' roots under the smaller (atomicMin: no retry loop under
+// contention, unlike CAS unions on popular roots), then every vertex jumps to its root; rounds
+// repeat until no hook changes anything.  The edges are walked a warp per 32-row group over the
+// group's contiguous arcs (each arc's row found by a shuffle search over the group's row_ptr).
+namespace cgk = cooperative_groups;
+__global__ void k_cc_sv(const int32_t *__restrict__ rp, const int32_t *__restrict__ col, int V, int32_t *f,
+                        int32_t *flags) {
+    cgk::grid_group grid = cgk::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gwarp = gtid >> 5, nwarps = nth >> 5;
+    const int64_t ngroups = ((int64_t)V + 31) >> 5;
+    for (int64_t v = gtid; v < V; v += nth) f[v] = (int)v;
+    if (gtid == 0) flags[0] = flags[1] = flags[2] = 0;
+    grid.sync();
+    for (int it = 0;; ++it) {
+        // three rotating flags: the one reset here was last read two rounds ago, before the
+        // grid barriers of the previous round
+        int32_t *fl = flags + (it % 3);
+        if (gtid == 0) flags[(it + 1) % 3] = 0;
+        bool changed = false;
+        for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+            const int r0 = (int)(g * 32);
+            const int rl = r0 + lane < V ? r0 + lane : V;
+            const int rpl = rp[rl];                                  // lane t: first arc of row r0 + t
+            const int A0 = __shfl_sync(0xffffffffu, rpl, 0);
+            const int A1 = rp[r0 + 32 < V ? r0 + 32 : V];
+            for (int base = A0; base < A1; base += 32) {              // warp-uniform trip count
+                const int j = base + lane;
+                const bool ok = j < A1;
+                // row of arc j: the last lane t with rp[r0 + t] <= j (5-step shuffle search)
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int x = __shfl_sync(0xffffffffu, rpl, lo + step);
+                    if (lo + step < 32 && x <= j) lo += step;
+                }
+                if (!ok) continue;
+                const int u = r0 + lo, w = col[j];
+                if (w <= u) continue;                                 // each edge once
+                const int fu = f[u], fw = f[w];
+                if (fu == fw) continue;
+                const int hi = fu > fw ? fu : fw, lw = fu > fw ? fw : fu;
+                if (atomicMin(f + hi, lw) > lw) changed = true;
+            }
+        }
+        if (changed) *fl = 1;
+        grid.sync();
+        for (int64_t v = gtid; v < V; v += nth) {                     // jump to the root
+            int x = f[v];
+            int y = f[x];
+            while (x != y) {
+                x = y;
+                y = f[x];
+            }
+            f[v] = x;
+        }
+        grid.sync();
+        if (*((volatile int32_t *)fl) == 0) break;
     }
 }
 
@@ -732,6 +799,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     HM_CUDA(cudaMemsetAsync(scal.p, 0, 64, s));
     HM_CUDA(cudaMemsetAsync(csize.p, 0, csize.bytes, s));
 
+    cudaEvent_t ph = phase_begin(ctx);
     Prune pr;
     const int32_t *rem = nullptr;
     const int heavy_param = ctx->params.bfs_heavy;
@@ -755,11 +823,28 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
                                               h_heavy_small > 0 ? hstart.as<int32_t>() : nullptr);
         check_launch("k_small_prep");
         count_launch(ctx);
+        phase_end(ctx, PH_RELABEL, ph);
+        ph = phase_begin(ctx);
     } else {
     // 1. connected components
-    if (ctx->params.cc_init == 1) k_cc_init<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
+    if (ctx->params.cc_init == 3) {
+        // one cooperative launch (grid: what fits, at most 4 CTAs per SM)
+        int per_sm = 0;
+        HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cc_sv, TB, 0));
+        if (per_sm > 4) per_sm = 4;
+        HM_REQUIRE(per_sm >= 1, HM_ECUDA, "k_cc_sv occupancy");
+        int gc = (int)grid_for((int64_t)V * 2, TB, (int64_t)ctx->num_sms * per_sm);
+        int32_t *fp = parent.as<int32_t>();
+        int32_t *flg = scalars + 12;                                  // zeroed scalars block, [12..14]
+        const int32_t *rpp = U.rp, *clp = U.col;
+        int Vv = V;
+        void *args[] = {(void *)&rpp, (void *)&clp, (void *)&Vv, (void *)&fp, (void *)&flg};
+        HM_CUDA(cudaLaunchCooperativeKernel((const void *)k_cc_sv, dim3(gc), dim3(TB), args, 0, s));
+        count_launch(ctx);
+    } else if (ctx->params.cc_init == 1) k_cc_init<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
     else k_iota<<<gb, TB, 0, s>>>(parent.as<int32_t>(), V);
-    if (ctx->params.cc_init == 2) {
+    if (ctx->params.cc_init == 3) {
+    } else if (ctx->params.cc_init == 2) {
         // csize doubles as the root-count scratch; scalars + 8 (zeroed) holds the giant pick
         unsigned long long *gbest = reinterpret_cast<unsigned long long *>(scalars + 8);
         k_cc_sample<<<gb, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
@@ -774,11 +859,15 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     k_cc_compress<<<gb, TB, 0, s>>>(parent.as<int32_t>(), label.as<int32_t>(), csize.as<int32_t>(), V);
     check_launch("cc");
     count_launch(ctx, 3);
+    phase_end(ctx, PH_CC, ph);
+    ph = phase_begin(ctx);
 
     // 1b. exact 2-core pruning of the largest component (prune.cu; single graph only)
     if (want_prune && gs.size() == 1)
         prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr);
     rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
+    phase_end(ctx, PH_PRUNE, ph);
+    ph = phase_begin(ctx);
 
     if (d_S_total) {
         Graph &G = *gs[0];
@@ -787,6 +876,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         if (pr.active) prune_finish(ctx, pr, label.as<int32_t>(), csize.as<int32_t>(), Sfin.as<uint64_t>(), V);
         finalize_graph(ctx, G, nullptr, label.as<int32_t>(), csize.as<int32_t>(), nullptr, scalars,
                        Sfin.as<uint64_t>(), 0);
+        phase_end(ctx, PH_FINALIZE, ph);
         return;
     }
 
@@ -833,6 +923,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
                                      heavy.as<int32_t>(), scalars, rem, V);
     check_launch("k_relabel_cols");
     count_launch(ctx, 2);
+    phase_end(ctx, PH_RELABEL, ph);
+    ph = phase_begin(ctx);
 
     if (ctx->params.bfs_dbg & 2) {
         if (!ctx->dbgc.p) ctx->dbgc.alloc(335872 * 8, s);
@@ -995,6 +1087,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cudaMemsetAsync(ctx->dbgc.p, 0, 139264 * 8, s));
         a.dbgc = ctx->dbgc.as<unsigned long long>();
     }
+    phase_end(ctx, PH_BFS_SETUP, ph);
+    ph = phase_begin(ctx);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->params.timing) {
         HM_CUDA(cudaEventCreate(&e0));
@@ -1021,6 +1115,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     }
     count_launch(ctx);
     ctx->stats.bfs_launches += 1;
+    phase_end(ctx, PH_BFS, ph);
+    ph = phase_begin(ctx);
 
     if (small) {
         Graph &G = *gs[0];
@@ -1034,6 +1130,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         check_launch("k_small_finish");
         count_launch(ctx);
         G.has_results = true;
+        phase_end(ctx, PH_FINALIZE, ph);
         return;
     }
     if (d_S_partial) {
@@ -1041,6 +1138,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
                                                                                  scalars, d_S_partial, V);
         check_launch("k_partial_sums");
         count_launch(ctx);
+        phase_end(ctx, PH_FINALIZE, ph);
         return;
     }
     if (gs.size() == 1) {
@@ -1054,6 +1152,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         if (pr.active) prune_finish(ctx, pr, label.as<int32_t>(), csize.as<int32_t>(), Sfin.as<uint64_t>(), V);
         finalize_graph(ctx, *gs[0], nullptr, label.as<int32_t>(), csize.as<int32_t>(), nullptr, scalars,
                        Sfin.as<uint64_t>(), 0);
+        phase_end(ctx, PH_FINALIZE, ph);
         return;
     }
     for (size_t gi = 0; gi < gs.size(); ++gi)

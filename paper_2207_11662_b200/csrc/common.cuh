@@ -93,7 +93,8 @@ struct Params {
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_fbar = 1;          // MS-BFS level barrier with the any-change flag folded in
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
-    int cc_init = 2;           // components: 0 union over all arcs, 1 from parent = smallest neighbour, 2 sampled (Afforest)
+    int cc_init = 3;           // components: 0 union over all arcs, 1 from parent = smallest neighbour, 2 sampled
+                               // (Afforest), 3 min-label hooking + pointer jumping in one cooperative launch
     int bfs_unit = 0;          // MS-BFS light-path rows per work unit (0 = auto by rows per warp; 32 ... 2)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level
@@ -125,11 +126,32 @@ struct hm_ctx {
     int num_sms = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;   // MS-BFS launch events (timing=1)
+    struct PhaseEv { int id; cudaEvent_t e0, e1; };
+    std::vector<PhaseEv> phase_pending;                          // per-phase events (timing=2)
+    double phase_ms[10] = {0};
 };
 
 namespace hm {
 
 inline void count_launch(hm_ctx *ctx, int n = 1) { ctx->stats.launches += n; }
+
+// per-phase CUDA-event timing (param timing >= 2; resolved in hm_get_stats, no synchronisation here)
+enum { PH_CC = 0, PH_PRUNE, PH_RELABEL, PH_BFS_SETUP, PH_BFS, PH_FINALIZE, PH_COMPOSE, PH_TOPK, PH_AGGREGATE, PH_OTHER };
+inline cudaEvent_t phase_begin(hm_ctx *ctx) {
+    if (ctx->params.timing < 2) return nullptr;
+    cudaEvent_t e;
+    HM_CUDA(cudaEventCreate(&e));
+    HM_CUDA(cudaEventRecord(e, ctx->stream));
+    return e;
+}
+inline void phase_end(hm_ctx *ctx, int id, cudaEvent_t &e0) {
+    if (!e0) return;
+    cudaEvent_t e1;
+    HM_CUDA(cudaEventCreate(&e1));
+    HM_CUDA(cudaEventRecord(e1, ctx->stream));
+    ctx->phase_pending.push_back({id, e0, e1});
+    e0 = nullptr;
+}
 
 // a host round trip inside a library call (counted: a step without any can be captured in a CUDA graph)
 inline void host_sync(hm_ctx *ctx) {

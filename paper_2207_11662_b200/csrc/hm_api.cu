@@ -107,6 +107,10 @@ void hm_destroy(hm_ctx *ctx) {
         cudaEventDestroy(pe.first);
         cudaEventDestroy(pe.second);
     }
+    for (auto &pe : ctx->phase_pending) {
+        cudaEventDestroy(pe.e0);
+        cudaEventDestroy(pe.e1);
+    }
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -134,7 +138,7 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_prune must be 0, 1 or 2 (auto)");
         ctx->params.bfs_prune = (int)value;
     } else if (n == "cc_init") {
-        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "cc_init must be 0, 1 or 2");
+        HM_REQUIRE(value >= 0 && value <= 3, HM_EINVAL, "cc_init must be 0, 1, 2 or 3");
         ctx->params.cc_init = (int)value;
     } else if (n == "bfs_fbar") {
         ctx->params.bfs_fbar = value ? 1 : 0;
@@ -162,7 +166,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_dbg") {
         ctx->params.bfs_dbg = (int)value;
     } else if (n == "timing") {
-        ctx->params.timing = value ? 1 : 0;
+        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "timing must be 0, 1 or 2");
+        ctx->params.timing = (int)value;
     } else {
         throw Error(HM_EINVAL, "unknown parameter " + n);
     }
@@ -224,7 +229,9 @@ static hm_status aggregate(hm_ctx *ctx, const int32_t *ids, int32_t r, int32_t *
     for (int i = 0; i < r; ++i) in.push_back(&graph(ctx, ids[i]));
     for (int i = 1; i < r; ++i) HM_REQUIRE(in[i]->V == in[0]->V, HM_EINVAL, "graphs differ in V");
     Graph out;
+    cudaEvent_t ph = phase_begin(ctx);
     and_or_aggregate(ctx, in, is_and, out);
+    phase_end(ctx, PH_AGGREGATE, ph);
     // reuse a freed slot, else append (pointers in `in` are not used after this)
     int32_t slot = -1;
     for (int32_t i = ctx->n_layers; i < (int32_t)ctx->graphs.size(); ++i)
@@ -355,8 +362,10 @@ hm_status hm_topk_closeness(hm_ctx *ctx, int32_t g, int32_t K, int32_t *ids_out)
     HM_REQUIRE(K >= 1 && K <= G.V, HM_EINVAL, "K must be in [1, V]");
     HM_REQUIRE(ids_out, HM_EINVAL, "null ids_out");
     Buf keys((size_t)G.V * 8, ctx->stream), ids((size_t)K * 4, ctx->stream);
+    cudaEvent_t ph = phase_begin(ctx);
     closeness_desc_keys(ctx, G.c.as<double>(), G.V, keys.as<uint64_t>());
     topk(ctx, keys.as<uint64_t>(), G.V, K, ids.as<int32_t>());
+    phase_end(ctx, PH_TOPK, ph);
     copy_out(ctx, ids_out, ids.p, (size_t)K * 4);
     HM_API_END(ctx)
 }
@@ -373,7 +382,9 @@ hm_status hm_compose(hm_ctx *ctx, int32_t heuristic, const int32_t *layer_ids, i
     HM_REQUIRE((int32_t)seen.size() == r, HM_EINVAL, "repeated graph id");
     std::vector<Graph *> gs;
     for (int i = 0; i < r; ++i) gs.push_back(&graph(ctx, layer_ids[i]));
+    cudaEvent_t ph = phase_begin(ctx);
     compose(ctx, heuristic, gs, K, ids_out, count_out);
+    phase_end(ctx, PH_COMPOSE, ph);
     HM_API_END(ctx)
 }
 
@@ -464,6 +475,15 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
         cudaEventDestroy(pe.second);
     }
     ctx->pending.clear();
+    for (auto &pe : ctx->phase_pending) {
+        float ms = 0.f;
+        HM_CUDA(cudaEventElapsedTime(&ms, pe.e0, pe.e1));
+        ctx->phase_ms[pe.id] += ms;
+        cudaEventDestroy(pe.e0);
+        cudaEventDestroy(pe.e1);
+    }
+    ctx->phase_pending.clear();
+    for (int i = 0; i < 10; ++i) out->phase_ms[i] = ctx->phase_ms[i];
     out->launches = ctx->stats.launches;
     out->host_syncs = ctx->stats.host_syncs;
     out->bfs_launches = ctx->stats.bfs_launches;
@@ -477,6 +497,7 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     out->bfs_state_bytes = (double)dv[6];
     if (reset) {
         ctx->stats = Stats();
+        for (int i = 0; i < 10; ++i) ctx->phase_ms[i] = 0.0;
         HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));
         HM_CUDA(cudaStreamSynchronize(ctx->stream));
     }

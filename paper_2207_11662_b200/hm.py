@@ -99,7 +99,9 @@ class Context:
     def stats(self, reset=False):
         s = _lib.HmStats()
         self._check(self.L.hm_get_stats(self.h, ctypes.byref(s), 1 if reset else 0))
-        return {k: getattr(s, k) for k, _ in _lib.HmStats._fields_}
+        out = {k: getattr(s, k) for k, _ in _lib.HmStats._fields_}
+        out["phase_ms"] = list(s.phase_ms)
+        return out
 
     # ------------------------------------------------------------- graphs
     def load_layers(self, V, layers):
