@@ -75,7 +75,7 @@ const char *hm_last_error(const hm_ctx *ctx);
  *              flag; 1 (default) one counter atomic per CTA carries both (arrival and "row changed")
  *   "bfs_hints"   : MS-BFS L2 eviction-priority bits (1 gathers evict_last, 2 own F_{d-2} evict_first,
  *                   4 F_d stores evict_last, 8 F_d stores evict_first; default 11)
- *   "cc_init"     : connected components: 3 (default) min-label hooking (atomicMin of the larger root
+ *   "cc_init"     : connected components: 4 (default) = 3 from V = 32768, else 2; 3 min-label hooking (atomicMin of the larger root
  *                   under the smaller) and pointer jumping, rounds until no hook changes, in one
  *                   cooperative launch; 2 sampled union-find (unite each vertex with its first 2
  *                   neighbours, then only rows outside the most frequent root unite over the rest);

@@ -826,8 +826,10 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         phase_end(ctx, PH_RELABEL, ph);
         ph = phase_begin(ctx);
     } else {
-    // 1. connected components
-    if (ctx->params.cc_init == 3) {
+    // 1. connected components (auto: the one-launch hooking pays from V = 32768 -- C5 layer 0.2 vs
+    // 0.5-1.0 ms -- while its grid barriers cost more than they save on C2-sized graphs, 0.51 vs 0.30 ms)
+    const int cc_init = ctx->params.cc_init == 4 ? (V >= 32768 ? 3 : 2) : ctx->params.cc_init;
+    if (cc_init == 3) {
         // one cooperative launch (grid: what fits, at most 4 CTAs per SM)
         int per_sm = 0;
         HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cc_sv, TB, 0));
@@ -841,10 +843,10 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         void *args[] = {(void *)&rpp, (void *)&clp, (void *)&Vv, (void *)&fp, (void *)&flg};
         HM_CUDA(cudaLaunchCooperativeKernel((const void *)k_cc_sv, dim3(gc), dim3(TB), args, 0, s));
         count_launch(ctx);
-    } else if (ctx->params.cc_init == 1) k_cc_init<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
+    } else if (cc_init == 1) k_cc_init<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
     else k_iota<<<gb, TB, 0, s>>>(parent.as<int32_t>(), V);
-    if (ctx->params.cc_init == 3) {
-    } else if (ctx->params.cc_init == 2) {
+    if (cc_init == 3) {
+    } else if (cc_init == 2) {
         // csize doubles as the root-count scratch; scalars + 8 (zeroed) holds the giant pick
         unsigned long long *gbest = reinterpret_cast<unsigned long long *>(scalars + 8);
         k_cc_sample<<<gb, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);

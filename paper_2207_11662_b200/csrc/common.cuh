@@ -93,8 +93,9 @@ struct Params {
     int bfs_interleave = 1;    // MS-BFS: CTAs own interleaved units (1) or contiguous ranges (0)
     int bfs_fbar = 1;          // MS-BFS level barrier with the any-change flag folded in
     int bfs_hints = 11;        // MS-BFS L2 eviction-priority bits (msbfs.cuh BfsArgs::hints)
-    int cc_init = 3;           // components: 0 union over all arcs, 1 from parent = smallest neighbour, 2 sampled
-                               // (Afforest), 3 min-label hooking + pointer jumping in one cooperative launch
+    int cc_init = 4;           // components: 0 union over all arcs, 1 from parent = smallest neighbour, 2 sampled
+                               // (Afforest), 3 min-label hooking + pointer jumping in one cooperative launch,
+                               // 4 (default) = 3 from V = 32768, else 2
     int bfs_unit = 0;          // MS-BFS light-path rows per work unit (0 = auto by rows per warp; 32 ... 2)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level

@@ -138,7 +138,7 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_prune must be 0, 1 or 2 (auto)");
         ctx->params.bfs_prune = (int)value;
     } else if (n == "cc_init") {
-        HM_REQUIRE(value >= 0 && value <= 3, HM_EINVAL, "cc_init must be 0, 1, 2 or 3");
+        HM_REQUIRE(value >= 0 && value <= 4, HM_EINVAL, "cc_init must be 0, 1, 2, 3 or 4 (auto)");
         ctx->params.cc_init = (int)value;
     } else if (n == "bfs_fbar") {
         ctx->params.bfs_fbar = value ? 1 : 0;

@@ -559,7 +559,7 @@ def test_random_sweep_all_knobs(hm):
     rng = random.Random(20220722)
     knobs = dict(bfs_words=[0, 8, 16, 32, 64, 128], bfs_prune=[0, 1, 2], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
                  bfs_chg_smem=[0, 1], bfs_unit=[0, 2, 4, 8, 16, 32], bfs_heavy=[0, 2, 16, 256], bfs_blocks_per_sm=[0, 1],
-                 bfs_fbar=[0, 1], cc_init=[0, 1, 2, 3], bfs_td=[0, 2, 8, 32, 1 << 20])
+                 bfs_fbar=[0, 1], cc_init=[0, 1, 2, 3, 4], bfs_td=[0, 2, 8, 32, 1 << 20])
     with hm() as ctx:
         for t in range(200):
             V, E = _shape(rng, t)
