@@ -865,8 +865,11 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     ph = phase_begin(ctx);
 
     // 1b. exact 2-core pruning of the largest component (prune.cu; single graph only)
-    if (want_prune && gs.size() == 1)
-        prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr);
+    if (want_prune && gs.size() == 1) {
+        Graph &G0 = *gs[0];
+        PruneDecision *dec = G0.and_key.empty() ? &G0.pdec : &ctx->and_pdec[G0.and_key];
+        prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr, dec);
+    }
     rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
     phase_end(ctx, PH_PRUNE, ph);
     ph = phase_begin(ctx);

@@ -5,6 +5,7 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <map>
 #include <stdexcept>
 
 #include "../../include/hm.h"
@@ -68,6 +69,18 @@ struct Buf {
     template <class T> T *as() const { return static_cast<T *>(p); }
 };
 
+// The host-side outcome of the pruning round trip (prune.cu): a pure function of the graph, so it is
+// kept with the graph (layers: for their lifetime; AND aggregates: keyed by their layer set until
+// the next hm_load_layers) and later closeness calls skip the round trip.  All device work
+// (peeling, relabelling, the BFS) still runs on every call.
+struct PruneDecision {
+    bool valid = false;
+    bool active = false;
+    int P = -1, R = 0, peeled = 0;
+    int maxdeg = 0, nonisolated = 0;
+    int64_t arcs = 0;
+};
+
 // ------------------------------------------------------- per-graph state
 struct Graph {
     bool alive = false;
@@ -82,6 +95,8 @@ struct Graph {
     Buf S, k, c, pen, deg, ch;   // uint64, int32, double, uint64, int32, uint32 bitmap
     double mu = 0.0;
     int32_t ch_count = 0;
+    PruneDecision pdec;              // cached pruning decision (see PruneDecision)
+    std::vector<int32_t> and_key;    // AND aggregates: the sorted layer ids (decision cache key)
 };
 
 struct Params {
@@ -119,6 +134,7 @@ struct hm_ctx {
     bool own_stream = false;
     std::string err;
     std::vector<hm::Graph> graphs;
+    std::map<std::vector<int32_t>, hm::PruneDecision> and_pdec;   // AND graphs' pruning decisions by layer set
     int32_t n_layers = 0;
     hm::Params params;
     hm::Stats stats;
@@ -209,7 +225,7 @@ struct Prune {
     Buf rem, par, tsz, tD, degl, lsize, Cc, scal;   // per vertex / per component root
 };
 bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const int32_t *label, const int32_t *csize,
-                     int V, Prune &pr);
+                     int V, Prune &pr, PruneDecision *dec);
 void prune_finish(hm_ctx *ctx, Prune &pr, const int32_t *label, const int32_t *csize, uint64_t *S_orig, int V);
 void closeness_combine(hm_ctx *ctx, Graph &G, const uint64_t *d_S_total);
 // exact (correctly rounded) sum of masked non-negative doubles, then mean = sum / count;

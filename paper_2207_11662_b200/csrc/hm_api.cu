@@ -194,6 +194,7 @@ hm_status hm_load_layers(hm_ctx *ctx, int32_t V, int32_t l, const int32_t *const
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->graphs = std::move(gs);
     ctx->n_layers = l;
+    ctx->and_pdec.clear();                 // decisions of AND aggregates of the previous layers
     if (dropped_out)
         for (int i = 0; i < l; ++i) dropped_out[i] = dropped[i];
     HM_API_END(ctx)
@@ -232,6 +233,14 @@ static hm_status aggregate(hm_ctx *ctx, const int32_t *ids, int32_t r, int32_t *
     cudaEvent_t ph = phase_begin(ctx);
     and_or_aggregate(ctx, in, is_and, out);
     phase_end(ctx, PH_AGGREGATE, ph);
+    if (is_and) {   // the aggregate is a function of its layer set: the key of its cached decisions
+        bool layers_only = true;
+        for (int i = 0; i < r; ++i) layers_only = layers_only && ids[i] < ctx->n_layers;
+        if (layers_only) {
+            out.and_key.assign(ids, ids + r);
+            std::sort(out.and_key.begin(), out.and_key.end());
+        }
+    }
     // reuse a freed slot, else append (pointers in `in` are not used after this)
     int32_t slot = -1;
     for (int32_t i = ctx->n_layers; i < (int32_t)ctx->graphs.size(); ++i)

@@ -172,7 +172,7 @@ int coop_grid(const void *kern, int threads, int num_sms) {
 }  // namespace
 
 bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const int32_t *label, const int32_t *csize,
-                     int V, Prune &pr) {
+                     int V, Prune &pr, PruneDecision *dec) {
     cudaStream_t s = ctx->stream;
     pr.active = false;
     if (V < 3) return false;
@@ -207,30 +207,42 @@ bool prune_component(hm_ctx *ctx, const int32_t *rp, const int32_t *col, const i
     k_graph_stats<<<gb, TB, 0, s>>>(rp, V, scal + 10);
     check_launch("k_graph_stats");
     count_launch(ctx, 4);
-    // one host round trip decides whether the pruned BFS pays (and brings the graph's shape along)
-    struct {
-        int32_t R, peeled, f0, f1, lsizeP_unused, max_other, maxT, pad;
-        unsigned long long best;
-        int32_t maxdeg, nonisolated, arcs, pad2;
-    } h;
-    HM_CUDA(cudaMemcpyAsync(&h, pr.scal.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    host_sync(ctx);
-    const int P = V - 1 - (int)(h.best & 0xffffffffull);
-    const int sizeP = (int)(h.best >> 32);
-    const int coreP = sizeP - h.peeled;
-    pr.R = h.R;
-    pr.peeled = h.peeled;
-    pr.P = P;
+    PruneDecision d;
+    if (dec && dec->valid) {
+        d = *dec;                        // decided by an earlier call on the same graph: no round trip
+    } else {
+        // one host round trip decides whether the pruned BFS pays (and brings the graph's shape along)
+        struct {
+            int32_t R, peeled, f0, f1, lsizeP_unused, max_other, maxT, pad;
+            unsigned long long best;
+            int32_t maxdeg, nonisolated, arcs, pad2;
+        } h;
+        HM_CUDA(cudaMemcpyAsync(&h, pr.scal.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        host_sync(ctx);
+        const int sizeP = (int)(h.best >> 32);
+        const int coreP = sizeP - h.peeled;
+        d.valid = true;
+        d.P = V - 1 - (int)(h.best & 0xffffffffull);
+        d.R = h.R;
+        d.peeled = h.peeled;
+        d.maxdeg = h.maxdeg;
+        d.nonisolated = h.nonisolated;
+        d.arcs = h.arcs;
+        // worth it: >= 1 % of P peeled; P's core still the strictly largest live component
+        // (so it stays the first, "giant" batch component); T fits the kernel's bit planes
+        d.active = h.peeled > 0 && (int64_t)h.peeled * 100 >= sizeP && coreP > h.max_other &&
+                   h.maxT < (1 << BFS_T_BITS);
+        if (dec) *dec = d;
+    }
+    pr.R = d.R;
+    pr.peeled = d.peeled;
+    pr.P = d.P;
     pr.shape_known = true;
-    pr.maxdeg = h.maxdeg;
-    pr.nonisolated = h.nonisolated;
-    pr.arcs = h.arcs;
-    // worth it: >= 1 % of P peeled; P's core still the strictly largest live component
-    // (so it stays the first, "giant" batch component); T fits the kernel's bit planes
-    pr.active = h.peeled > 0 && (int64_t)h.peeled * 100 >= sizeP && coreP > h.max_other &&
-                h.maxT < (1 << BFS_T_BITS);
-    if (!pr.active) return false;
-    return true;
+    pr.maxdeg = d.maxdeg;
+    pr.nonisolated = d.nonisolated;
+    pr.arcs = d.arcs;
+    pr.active = d.active;
+    return pr.active;
 }
 
 void prune_finish(hm_ctx *ctx, Prune &pr, const int32_t *label, const int32_t *csize, uint64_t *S_orig, int V) {
