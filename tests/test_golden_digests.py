@@ -24,5 +24,6 @@ def test_golden_digests_cover_every_config():
         assert gold["input_sha256"] == input_sha(h)
         assert [w["T"] for w in gold["ands"]] == [list(T) for T in h.subsets]
         assert len(gold["layers"]) == len(h.layers)
+        assert all("or_edges" in w and "cc1_ranked" in w and "gt_topk" in w for w in gold["ands"])
 
 

@@ -10,10 +10,11 @@ layouts of tests/_digest.py, keyed by the SHA-256 of the inputs.  Compared
 bit-exactly here:
   * per layer and per AND subset: S, k, closeness (IEEE bits), n-penalty sums,
     degrees, the CC-node set and its mean mu (PAPER.md:186, :209, :431);
-  * per subset: the AND edge set, the ground-truth top-K
+  * per subset: the AND and OR edge sets, the ground-truth top-K
     (PAPER.md:205-209), CC2 top-K (Alg. 1), CC1's whole ranked set R (K = V;
     Eq. 2-3 and the pseudocode), the naive set
-    and the CC2 above-average set (PAPER.md:593);
+    and the CC2 above-average set, and the accuracy metrics of each heuristic's
+    top-K against the GT top-K (PAPER.md:372);
   * mu == math.fsum(c) / V on the GPU's own closeness values (Z6).
 """
 import json
@@ -108,7 +109,24 @@ def test_fullsize_config(Context, name, knobs):
             assert nn == want["naive_n"] and sha(idsn, "ids") == want["naive"], tag
             idsa, na = ctx.compose("cc2_avg", T, V)
             assert na == want["cc2_avg_n"] and sha(idsa, "ids") == want["cc2_avg"], tag
+            # the paper's evaluation: each heuristic's top-K against the GT top-K, on the
+            # GPU's lists and set-metric kernel vs the oracle's plain Jaccard / P / R / F1 of its lists
+            gt = ctx.topk_closeness(g, K)
+            for heur, key in (("cc2", "cc2_topk"), (cc1_name(T), "cc1_topk"), ("naive", "naive_topk")):
+                est, _ = ctx.compose(heur, T, K)
+                m = ctx.set_metrics(V, est, gt)
+                p_, r_, f_ = O.prf1(want[key], want["gt_topk"])
+                assert (m["jaccard"], m["precision"], m["recall"], m["f1"]) == \
+                    (O.jaccard(want[key], want["gt_topk"]), p_, r_, f_), (tag, heur)
             ctx.free_graph(g)
+            # OR aggregation: the edge set
+            go = ctx.or_aggregate(T)
+            rp, col = ctx.graph_csr(go)
+            src = np.repeat(np.arange(V, dtype=np.int64), np.diff(rp))
+            keep = src < col
+            keys = np.sort(src[keep] * V + col[keep])
+            assert len(keys) == want["or_m"] and sha(keys, "edges") == want["or_edges"], tag + " OR"
+            ctx.free_graph(go)
 
 
 def test_large_vertex_count(Context):

@@ -70,6 +70,9 @@ def golden(name, threads):
         rec["T"] = T
         rec["m"] = len(A)
         rec["edges"] = sha(edge_keys(V, A), "edges")
+        Or = O.or_aggregate([Es[i] for i in T])
+        rec["or_m"] = len(Or)
+        rec["or_edges"] = sha(edge_keys(V, Or), "edges")
         rec["gt_topk"] = O.topk_closeness(ra["c"], K)
         rec["cc2_topk"] = O.cc2(rs, K)[0]
         r1, n1, _ = O.cc1(rs, V)                          # the full ranked set R (K = V)
@@ -93,13 +96,34 @@ def golden(name, threads):
     print(f"[{name}] wrote {path} ({out['oracle_seconds']} s)", flush=True)
 
 
+def add_or(name):
+    """add the OR aggregate's edge-set digest of every subset (oracle or_aggregate) to an
+    existing digest file without re-running the BFS."""
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_{name}.json")
+    out = json.load(open(path))
+    h = build_config(name)
+    assert out["input_sha256"] == input_sha(h)
+    Es = [set(map(tuple, L.tolist())) for L in h.layers]
+    for rec in out["ands"]:
+        A = O.or_aggregate([Es[i] for i in rec["T"]])
+        rec["or_m"] = len(A)
+        rec["or_edges"] = sha(edge_keys(V=h.V, pairs=A), "edges")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(f"[{name}] OR digests added to {path}", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--add-or", action="store_true", help="only add the OR edge-set digests to existing files")
     a = ap.parse_args()
     for c in a.configs:
-        golden(c, a.threads)
+        if a.add_or:
+            add_or(c)
+        else:
+            golden(c, a.threads)
 
 
 if __name__ == "__main__":
