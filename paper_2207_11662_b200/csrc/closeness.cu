@@ -211,27 +211,26 @@ __global__ void k_cc_compress(int32_t *p, int32_t *label, int32_t *csize, int V)
     }
 }
 
-// component keys: roots -> ((V - size) << sh | root); others -> V << sh (sort last); sh = bits of V
-__global__ void k_comp_keys(const int32_t *label, const int32_t *csize, uint64_t *key, int V, int sh) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-        key[v] = (label[v] == v) ? (((uint64_t)(V - csize[v]) << sh) | (uint32_t)v)
-                                 : ((uint64_t)V << sh);
+// component keys (stable 32-bit key/value radix sort; ids ascending within equal keys):
+// roots -> key V - size, value root; others -> key V (sort last)
+__global__ void k_comp_keys(const int32_t *label, const int32_t *csize, uint32_t *key, uint32_t *val, int V) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        key[v] = (label[v] == v) ? (uint32_t)(V - csize[v]) : (uint32_t)V;
+        val[v] = (uint32_t)v;
+    }
 }
 
 // sorted component table; scalars[1] = n_giant (if > 1), scalars[2] = n_comp
-__global__ void k_comp_tables(const uint64_t *keys, int32_t *size_s, int32_t *rank_of_root,
-                              int32_t *scalars, int V, int sh) {
-    const uint64_t lo = (1ull << sh) - 1ull;
+__global__ void k_comp_tables(const uint32_t *keys, const uint32_t *vals, int32_t *size_s, int32_t *rank_of_root,
+                              int32_t *scalars, int V) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        const uint64_t k = keys[i];
-        const bool valid = (k >> sh) < (uint64_t)V;
-        if (valid) {
-            const int sz = V - (int)(k >> sh);
-            const int root = (int)(k & lo);
+        const uint32_t k = keys[i];
+        if (k < (uint32_t)V) {
+            const int sz = V - (int)k;
             size_s[i] = sz;
-            rank_of_root[root] = i;
+            rank_of_root[vals[i]] = i;
             if (i == 0) scalars[1] = sz > 1 ? sz : 0;
-            const bool last = (i + 1 == V) || ((keys[i + 1] >> sh) >= (uint64_t)V);
+            const bool last = (i + 1 == V) || (keys[i + 1] >= (uint32_t)V);
             if (last) scalars[2] = i + 1;
         } else {
             size_s[i] = 0;
@@ -246,20 +245,22 @@ __global__ void k_nlive(const int32_t *size_s, const int32_t *cstart, int32_t *s
         if (size_s[i] > 1 && (i + 1 == n_comp || size_s[i + 1] <= 1)) scalars[0] = cstart[i] + size_s[i];
 }
 
-// peeled vertices (rem != nullptr, rem[v] > 0) sort after every component: no BFS row
-__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, const int32_t *rem, uint64_t *key,
-                            int V, int sh) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-        key[v] = ((rem && rem[v]) ? ((uint64_t)V << sh) : ((uint64_t)rank_of_root[label[v]] << sh)) | (uint32_t)v;
+// vertex keys: component rank (value: the vertex; the stable sort keeps ids ascending inside a
+// component); peeled vertices (rem[v] > 0) key V, after every component: no BFS row
+__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, const int32_t *rem, uint32_t *key,
+                            uint32_t *val, int V) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        key[v] = (rem && rem[v]) ? (uint32_t)V : (uint32_t)rank_of_root[label[v]];
+        val[v] = (uint32_t)v;
+    }
 }
 
-__global__ void k_perm(const uint64_t *keys, const int32_t *row_ptr, const int32_t *degl, const int32_t *size_s,
-                       const int32_t *cstart, int32_t *new_to_old, int32_t *old_to_new,
-                       int32_t *new_deg, int2 *cinfo, int V, int sh) {
+__global__ void k_perm(const uint32_t *rk, const uint32_t *olds, const int32_t *row_ptr, const int32_t *degl,
+                       const int32_t *size_s, const int32_t *cstart, int32_t *new_to_old, int32_t *old_to_new,
+                       int32_t *new_deg, int2 *cinfo, int V) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        const uint64_t k = keys[i];
-        const int old = (int)(k & ((1ull << sh) - 1ull));
-        const int r = (int)(k >> sh);
+        const int old = (int)olds[i];
+        const int r = (int)rk[i];
         new_to_old[i] = old;
         old_to_new[old] = i;
         if (r >= V) {                       // peeled vertex: no row
@@ -731,9 +732,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     int W = ctx->params.bfs_words > 0 ? ctx->params.bfs_words : 64;   // 0 = auto (64, or 128 below)
     const unsigned gb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
     const unsigned gw = grid_for((int64_t)V * 32, TB, (int64_t)ctx->num_sms * 16);
-    // sort keys (high << sh) | vertex with high <= V: sh = bits of V, 2 sh bits sorted
+    // sort keys are <= V: sh = bits of V (the small path packs (high << sh) | vertex in 2 sh bits)
     const int sh = nbits((uint64_t)V);
-    const int end_bit = 2 * sh;
 
     // per-graph outputs
     for (Graph *g : gs) {
@@ -887,32 +887,32 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
 
     // 2. component order and vertex order
     // (batching by live component sizes: the pruned component counts its core only)
+    // (stable 32-bit key / 32-bit value radix sorts over nbits(V) bits: 3 passes at V = 2^16..2^24
+    // instead of 64-bit composite keys over 2 nbits(V) bits)
+    uint32_t *kin = key1.as<uint32_t>(), *vin = kin + V, *kout = key2.as<uint32_t>(), *vout = kout + V;
     k_comp_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), pr.active ? pr.lsize.as<int32_t>() : csize.as<int32_t>(),
-                                  key1.as<uint64_t>(), V, sh);
+                                  kin, vin, V);
     count_launch(ctx);
     {
+        const int kbits = sh;                                      // keys <= V
         size_t tb = 0;
-        HM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
-                                               end_bit, s));
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, V, 0, kbits, s));
         size_t tb2 = 0;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, size_s.as<int32_t>(), cstart.as<int32_t>(), V + 1, s));
         if (tb2 > tb) tb = tb2;
         Buf tmp(tb, s);
-        HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
-                                               end_bit, s));
-        k_comp_tables<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), size_s.as<int32_t>(), rank.as<int32_t>(),
-                                       scalars, V, sh);
         size_t tbs = tb;
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tbs, kin, kout, vin, vout, V, 0, kbits, s));
+        k_comp_tables<<<gb, TB, 0, s>>>(kout, vout, size_s.as<int32_t>(), rank.as<int32_t>(), scalars, V);
+        tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, size_s.as<int32_t>(), cstart.as<int32_t>(), V, s));
         k_nlive<<<gb, TB, 0, s>>>(size_s.as<int32_t>(), cstart.as<int32_t>(), scalars, V);
-        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem, key1.as<uint64_t>(), V, sh);
+        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem, kin, vin, V);
         tbs = tb;
-        HM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tbs, key1.as<uint64_t>(), key2.as<uint64_t>(), V, 0,
-                                               end_bit, s));
-        k_perm<<<gb, TB, 0, s>>>(key2.as<uint64_t>(), U.rp, pr.active ? pr.degl.as<int32_t>() : nullptr,
-                                size_s.as<int32_t>(),
-                                cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
-                                ndeg.as<int32_t>(), cinfo.as<int2>(), V, sh);
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tbs, kin, kout, vin, vout, V, 0, kbits, s));
+        k_perm<<<gb, TB, 0, s>>>(kout, vout, U.rp, pr.active ? pr.degl.as<int32_t>() : nullptr,
+                                size_s.as<int32_t>(), cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
+                                ndeg.as<int32_t>(), cinfo.as<int2>(), V);
         tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, ndeg.as<int32_t>(), nrp.as<int32_t>(), V + 1, s));
         check_launch("relabel");
@@ -937,7 +937,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + 139264 * 8, n2o.p, nn * 4, cudaMemcpyDeviceToDevice, s));
         HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + (139264 + 65536) * 8, nrp.p, nn * 4,
                                 cudaMemcpyDeviceToDevice, s));
-        HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + (139264 + 2 * 65536) * 8, key2.p, nn * 8,
+        HM_CUDA(cudaMemcpyAsync(ctx->dbgc.as<char>() + (139264 + 2 * 65536) * 8, key2.p, nn * 4,
                                 cudaMemcpyDeviceToDevice, s));
     }
     }   // !small
