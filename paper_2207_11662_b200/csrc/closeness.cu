@@ -140,13 +140,20 @@ __global__ void k_cc_union(const int32_t *__restrict__ row_ptr, const int32_t *_
 // group's contiguous arcs (each arc's row found by a shuffle search over the group's row_ptr).
 namespace cgk = cooperative_groups;
 __global__ void k_cc_sv(const int32_t *__restrict__ rp, const int32_t *__restrict__ col, int V, int32_t *f,
-                        int32_t *flags) {
+                        int32_t *flags, int32_t *rowof) {
     cgk::grid_group grid = cgk::this_grid();
     const int lane = threadIdx.x & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int64_t gwarp = gtid >> 5, nwarps = nth >> 5;
+    const int64_t nnz = rp[V];
     const int64_t ngroups = ((int64_t)V + 31) >> 5;
+    // graphs with hub rows (rowof != null): the row of every arc (warp per row, coalesced writes), so
+    // the rounds walk the arcs evenly over all threads and a hub row does not hold one warp for
+    // thousands of arcs; otherwise a warp per 32-row group walks the group's contiguous arcs
+    if (rowof)
+        for (int64_t u = gwarp; u < V; u += nwarps)
+            for (int j = rp[u] + lane; j < rp[u + 1]; j += 32) rowof[j] = (int)u;
     for (int64_t v = gtid; v < V; v += nth) f[v] = (int)v;
     if (gtid == 0) flags[0] = flags[1] = flags[2] = 0;
     grid.sync();
@@ -156,29 +163,39 @@ __global__ void k_cc_sv(const int32_t *__restrict__ rp, const int32_t *__restric
         int32_t *fl = flags + (it % 3);
         if (gtid == 0) flags[(it + 1) % 3] = 0;
         bool changed = false;
-        for (int64_t g = gwarp; g < ngroups; g += nwarps) {
-            const int r0 = (int)(g * 32);
-            const int rl = r0 + lane < V ? r0 + lane : V;
-            const int rpl = rp[rl];                                  // lane t: first arc of row r0 + t
-            const int A0 = __shfl_sync(0xffffffffu, rpl, 0);
-            const int A1 = rp[r0 + 32 < V ? r0 + 32 : V];
-            for (int base = A0; base < A1; base += 32) {              // warp-uniform trip count
-                const int j = base + lane;
-                const bool ok = j < A1;
-                // row of arc j: the last lane t with rp[r0 + t] <= j (5-step shuffle search)
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int x = __shfl_sync(0xffffffffu, rpl, lo + step);
-                    if (lo + step < 32 && x <= j) lo += step;
-                }
-                if (!ok) continue;
-                const int u = r0 + lo, w = col[j];
+        if (rowof) {
+            for (int64_t j = gtid; j < nnz; j += nth) {
+                const int u = rowof[j], w = col[j];
                 if (w <= u) continue;                                 // each edge once
                 const int fu = f[u], fw = f[w];
                 if (fu == fw) continue;
                 const int hi = fu > fw ? fu : fw, lw = fu > fw ? fw : fu;
                 if (atomicMin(f + hi, lw) > lw) changed = true;
+            }
+        } else {
+            for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+                const int r0 = (int)(g * 32);
+                const int rl = r0 + lane < V ? r0 + lane : V;
+                const int rpl = rp[rl];                               // lane t: first arc of row r0 + t
+                const int A0 = __shfl_sync(0xffffffffu, rpl, 0);
+                const int A1 = rp[r0 + 32 < V ? r0 + 32 : V];
+                for (int base = A0; base < A1; base += 32) {          // warp-uniform trip count
+                    const int j = base + lane;
+                    // row of arc j: the last lane t with rp[r0 + t] <= j (5-step shuffle search)
+                    int lo = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int x = __shfl_sync(0xffffffffu, rpl, lo + step);
+                        if (lo + step < 32 && x <= j) lo += step;
+                    }
+                    if (j >= A1) continue;
+                    const int u = r0 + lo, w = col[j];
+                    if (w <= u) continue;                             // each edge once
+                    const int fu = f[u], fw = f[w];
+                    if (fu == fw) continue;
+                    const int hi = fu > fw ? fu : fw, lw = fu > fw ? fw : fu;
+                    if (atomicMin(f + hi, lw) > lw) changed = true;
+                }
             }
         }
         if (changed) *fl = 1;
@@ -840,7 +857,17 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         int32_t *flg = scalars + 12;                                  // zeroed scalars block, [12..14]
         const int32_t *rpp = U.rp, *clp = U.col;
         int Vv = V;
-        void *args[] = {(void *)&rpp, (void *)&clp, (void *)&Vv, (void *)&fp, (void *)&flg};
+        // arc-balanced rounds for graphs with hub rows (known from the graph's cached pruning round
+        // trip: C3's R-MAT layers 360-470 -> 190-250 us), row groups otherwise (C5 layers 0.23 vs 0.30 ms)
+        const PruneDecision *pd0 = gs.size() == 1 ? (gs[0]->and_key.empty() ? &gs[0]->pdec
+                                                     : (ctx->and_pdec.count(gs[0]->and_key)
+                                                            ? &ctx->and_pdec[gs[0]->and_key] : nullptr))
+                                                  : nullptr;
+        const bool hubs = pd0 && pd0->valid && pd0->maxdeg > 256;
+        Buf rowof;
+        if (hubs) rowof.alloc((size_t)(U.nnz > 0 ? U.nnz : 1) * 4, s);
+        int32_t *rop = hubs ? rowof.as<int32_t>() : nullptr;
+        void *args[] = {(void *)&rpp, (void *)&clp, (void *)&Vv, (void *)&fp, (void *)&flg, (void *)&rop};
         HM_CUDA(cudaLaunchCooperativeKernel((const void *)k_cc_sv, dim3(gc), dim3(TB), args, 0, s));
         count_launch(ctx);
     } else if (cc_init == 1) k_cc_init<<<gw, TB, 0, s>>>(U.rp, U.col, parent.as<int32_t>(), V);
