@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "exactsum.cuh"
 
 namespace hm {
 namespace {
@@ -49,24 +50,52 @@ __global__ void k_naive_keys(LayerPtrs L, int V, uint64_t *key, int32_t *count) 
 }
 
 // CC1 step 1 (Eq. 2): mindeg, ratio_i = pen_i / mindeg (+inf if mindeg = 0, Z8),
-// finite mask F
-__global__ void k_cc1_ratios(LayerPtrs L, int V, int32_t *mindeg, double *ratio, uint8_t *fin) {
+// fused with the exact sums of Eq. 3's layer averages (reading Z6: RN(exact sum) / count over
+// the finite ratios, Z8) and the zeroing of the main loop's counters and bitmap: one pass instead of
+// a ratio kernel, r exact-mean reductions and two memsets.  acc: r x EXACT_NLIMB zeroed 64-bit limbs,
+// then the finite count.  At most EXACT_MAX_PER_BLOCK vertices per block.
+__global__ void __launch_bounds__(256) k_cc1_ratios_sums(LayerPtrs L, int V, int32_t *mindeg, double *ratio,
+                                                         unsigned long long *acc, int32_t *icnt, uint32_t *R) {
+    __shared__ unsigned s16[RMAX][2 * EXACT_NLIMB];
+    __shared__ int s_cnt;
+    for (int i = threadIdx.x; i < L.r * 2 * EXACT_NLIMB; i += blockDim.x) s16[i / (2 * EXACT_NLIMB)][i % (2 * EXACT_NLIMB)] = 0u;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    int my = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         int md = L.deg[0][v];
         for (int i = 1; i < L.r; ++i) md = min(md, L.deg[i][v]);
         mindeg[v] = md;
-        fin[v] = md >= 1;
-        for (int i = 0; i < L.r; ++i)
-            ratio[(size_t)i * V + v] = md >= 1 ? __ddiv_rn((double)L.pen[i][v], (double)md) : (double)INFINITY;
+        icnt[v] = 0;
+        if ((v & 31) == 0) R[v >> 5] = 0u;
+        for (int i = 0; i < L.r; ++i) {
+            const double q = md >= 1 ? __ddiv_rn((double)L.pen[i][v], (double)md) : (double)INFINITY;
+            ratio[(size_t)i * V + v] = q;
+            if (md >= 1) exact_add16(s16[i], q);
+        }
+        my += md >= 1;
     }
+    my = __reduce_add_sync(0xffffffffu, my);
+    if ((threadIdx.x & 31) == 0 && my) atomicAdd(&s_cnt, my);
+    __syncthreads();
+    for (int i = threadIdx.x; i < L.r * EXACT_NLIMB; i += blockDim.x) {
+        const unsigned long long x = exact_limb16(s16[i / EXACT_NLIMB], i % EXACT_NLIMB);
+        if (x) atomicAdd(&acc[i], x);
+    }
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(&acc[(size_t)L.r * EXACT_NLIMB], (unsigned long long)s_cnt);
 }
 
-// Eq. 3: avgAND = max_i avg_i  (avg_i = 0 if no finite ratio)
-__global__ void k_cc1_avgand(const double *avgs, int r, double *avg_and) {
-    if (threadIdx.x != 0) return;
-    double m = avgs[0];
-    for (int i = 1; i < r; ++i) m = fmax(m, avgs[i]);
-    *avg_and = m;
+// avg_i = RN(exact sum of finite ratio_i) / |F| (0 if F is empty), then Eq. 3: avgAND = max_i avg_i
+__global__ void k_cc1_avgs(const unsigned long long *acc, int r, double *avgs) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long n = acc[(size_t)r * EXACT_NLIMB];
+    double m = 0.0;
+    for (int i = 0; i < r; ++i) {
+        const double a = n ? __ddiv_rn(exact_round(acc + (size_t)i * EXACT_NLIMB), (double)n) : 0.0;
+        avgs[i] = a;
+        m = i == 0 ? a : fmax(m, a);
+    }
+    avgs[r] = m;
 }
 
 __device__ __forceinline__ bool bsearch_row(const int32_t *__restrict__ col, int lo, int hi, int v) {
@@ -297,17 +326,19 @@ void compose(hm_ctx *ctx, int heuristic, const std::vector<Graph *> &gs, int32_t
         check_launch("cc2 above-average");
         count_launch(ctx, 2);
     } else if (heuristic == HM_CC1 || heuristic == HM_CC1_RARY) {
-        Buf mindeg((size_t)V * 4, s), ratio((size_t)V * r * 8, s), fin((size_t)V, s);
-        Buf avgs((size_t)(r + 1) * 8, s), R((size_t)((V + 31) / 32) * 4, s);
-        HM_CUDA(cudaMemsetAsync(R.p, 0, R.bytes, s));
-        k_cc1_ratios<<<g, TB, 0, s>>>(L, V, mindeg.as<int32_t>(), ratio.as<double>(), fin.as<uint8_t>());
-        count_launch(ctx);
-        for (int i = 0; i < r; ++i)
-            exact_mean(ctx, ratio.as<double>() + (size_t)i * V, V, fin.as<uint8_t>(), avgs.as<double>() + i,
-                       nullptr);
-        k_cc1_avgand<<<1, 32, 0, s>>>(avgs.as<double>(), r, avgs.as<double>() + r);
-        Buf icnt((size_t)V * 4, s);
-        HM_CUDA(cudaMemsetAsync(icnt.p, 0, icnt.bytes, s));
+        Buf mindeg((size_t)V * 4, s), ratio((size_t)V * r * 8, s);
+        Buf avgs((size_t)(r + 1) * 8, s), R((size_t)((V + 31) / 32) * 4, s), icnt((size_t)V * 4, s);
+        Buf acc(((size_t)r * EXACT_NLIMB + 1) * 8, s);
+        HM_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes, s));
+        int64_t nb = grid_for(V, TB, (int64_t)ctx->num_sms * 16);
+        const int64_t need = ((int64_t)V + EXACT_MAX_PER_BLOCK - 1) / EXACT_MAX_PER_BLOCK;
+        if (nb < need) nb = need;
+        // ratios (Eq. 2), the exact layer sums, zeroed counters and bitmap in one pass; then Eq. 3
+        k_cc1_ratios_sums<<<(unsigned)nb, TB, 0, s>>>(L, V, mindeg.as<int32_t>(), ratio.as<double>(),
+                                                     acc.as<unsigned long long>(), icnt.as<int32_t>(),
+                                                     R.as<uint32_t>());
+        k_cc1_avgs<<<1, 32, 0, s>>>(acc.as<unsigned long long>(), r, avgs.as<double>());
+        count_launch(ctx, 2);
         const int64_t nnz0 = gs[0]->nnz;
         const unsigned ga = grid_for(nnz0 > V ? nnz0 : (int64_t)V, TB, (int64_t)ctx->num_sms * 16);
         for (int pass = 0; pass < 2; ++pass)

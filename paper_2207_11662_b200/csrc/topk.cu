@@ -105,11 +105,22 @@ __global__ void k_gather(const uint64_t *__restrict__ keys, int n, SelState *st,
 // the 12th pass every block gathers its elements <= T.  (The multi-launch path below is kept for
 // grids the cooperative launch cannot place.)
 __global__ void __launch_bounds__(TB) k_select_coop(const uint64_t *__restrict__ keys, int n, SelState *st,
-                                                    uint64_t *ok, uint32_t *oid) {
+                                                    uint64_t *ok, uint32_t *oid, int K) {
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned h[256];
     __shared__ unsigned long long s_pkey;
     __shared__ unsigned s_pid;
+    if (blockIdx.x == 0) {                       // the selection state (no separate memset / init launches)
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) st->hist[i] = 0u;
+        if (threadIdx.x == 0) {
+            st->pkey = 0ull;
+            st->pid = 0u;
+            st->rem = K;
+            st->count = 0;
+            st->done = 0;
+        }
+    }
+    grid.sync();
     for (int p = 0; p < 12; ++p) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
         if (threadIdx.x == 0) {
@@ -270,8 +281,6 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
     }
     Buf stb(sizeof(SelState), s), ok((size_t)K * 8, s), oid((size_t)K * 4, s);
     SelState *st = stb.as<SelState>();
-    HM_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), s));
-    k_sel_init<<<1, 32, 0, s>>>(st, K);
     // one cooperative launch (grid: one CTA per 1 K keys, at most 4 per SM and what fits)
     int per_sm = 0;
     HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, TB, 0));
@@ -282,10 +291,13 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
         const uint64_t *kp = d_keys;
         uint64_t *okp = ok.as<uint64_t>();
         uint32_t *oip = oid.as<uint32_t>();
-        void *args[] = {(void *)&kp, (void *)&n, (void *)&st, (void *)&okp, (void *)&oip};
+        int Kk = K;
+        void *args[] = {(void *)&kp, (void *)&n, (void *)&st, (void *)&okp, (void *)&oip, (void *)&Kk};
         HM_CUDA(cudaLaunchCooperativeKernel((const void *)k_select_coop, dim3(gc), dim3(TB), args, 0, s));
-        count_launch(ctx, 2);
+        count_launch(ctx, 1);
     } else {
+        HM_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), s));
+        k_sel_init<<<1, 32, 0, s>>>(st, K);
         const unsigned g = grid_for(n, TB, (int64_t)ctx->num_sms * 4);
         for (int p = 0; p < 12; ++p) {
             k_hist<<<g, TB, 0, s>>>(d_keys, n, st, p);
