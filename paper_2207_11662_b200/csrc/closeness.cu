@@ -376,7 +376,14 @@ __global__ void k_union_copy(const int32_t *__restrict__ rp, const int32_t *__re
 __global__ void k_finalize(const int32_t *old_to_new, const int32_t *label, const int32_t *csize,
                            const int32_t *row_ptr, const uint64_t *S_rel, const int32_t *scalars,
                            const uint64_t *S_orig,
-                           uint64_t *S, int32_t *kk, double *c, uint64_t *pen, int32_t *deg, int V, int voff) {
+                           uint64_t *S, int32_t *kk, double *c, uint64_t *pen, int32_t *deg, int V, int voff,
+                           unsigned long long *acc, int32_t *cnt) {
+    // the exact sum of c for the mean (reading Z6): block-local 16-bit-half limbs, flushed to acc
+    // (at most EXACT_MAX_PER_BLOCK values per block)
+    __shared__ unsigned s16[2 * EXACT_NLIMB];
+    for (int i = threadIdx.x; i < 2 * EXACT_NLIMB; i += blockDim.x) s16[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = 0;
+    __syncthreads();
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         uint64_t s;
         if (S_orig) {
@@ -399,6 +406,36 @@ __global__ void k_finalize(const int32_t *old_to_new, const int32_t *label, cons
         c[v] = cv;
         pen[v] = s + (uint64_t)(V - k) * (uint64_t)V;   // n-penalty sum
         deg[v] = row_ptr[v + 1] - row_ptr[v];
+        exact_add16(s16, cv);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < EXACT_NLIMB; i += blockDim.x) {
+        const unsigned long long x = exact_limb16(s16, i);
+        if (x) atomicAdd(&acc[i], x);
+    }
+}
+
+// mu = RN(exact sum of c) / V (every block rounds the limbs itself; block 0 stores mu), then the CH
+// bitmap: bit v set iff c[v] > mu (strict), popcount into *count
+__global__ void k_mu_bitmap(const unsigned long long *acc, const double *c, uint32_t *bm, double *mu_out,
+                            int32_t *count, int V) {
+    __shared__ double s_mu;
+    if (threadIdx.x == 0) {
+        s_mu = __ddiv_rn(exact_round(acc), (double)V);
+        if (blockIdx.x == 0) *mu_out = s_mu;
+    }
+    __syncthreads();
+    const double m = s_mu;
+    const int lane = threadIdx.x & 31;
+    for (int64_t vb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31LL; vb < V;
+         vb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vb + lane;
+        const bool in = v < V && c[v] > m;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) {
+            bm[vb >> 5] = b;
+            if (b) atomicAdd(count, __popc(b));
+        }
     }
 }
 
@@ -412,21 +449,6 @@ __global__ void k_partial_sums(const int32_t *old_to_new, const uint64_t *S_rel,
     }
 }
 
-// CH bitmap: bit v set iff c[v] > mu (strict); popcount into *count
-__global__ void k_cc_bitmap(const double *c, const double *mu, uint32_t *bm, int32_t *count, int V) {
-    const int lane = threadIdx.x & 31;
-    const double m = *mu;
-    for (int64_t vb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31LL; vb < V;
-         vb += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = vb + lane;
-        const bool in = v < V && c[v] > m;
-        const unsigned b = __ballot_sync(0xffffffffu, in);
-        if (lane == 0) {
-            bm[vb >> 5] = b;
-            if (b) atomicAdd(count, __popc(b));
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------------------------
 // Small graphs (V <= SMALL_V, one graph, no pruning): the whole pre-processing (components,
@@ -695,21 +717,24 @@ static void finalize_graph(hm_ctx *ctx, Graph &G, const int32_t *o2n, const int3
                            const uint64_t *S_rel, const int32_t *scalars, const uint64_t *S_orig, int voff) {
     cudaStream_t s = ctx->stream;
     const int Vg = G.V;
-    k_finalize<<<grid_for(Vg, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(
-        o2n, label, csize, G.row_ptr.as<int32_t>(), S_rel, scalars, S_orig, G.S.as<uint64_t>(), G.k.as<int32_t>(),
-        G.c.as<double>(), G.pen.as<uint64_t>(), G.deg.as<int32_t>(), Vg, voff);
-    check_launch("k_finalize");
-    count_launch(ctx);
     uint32_t *chbm = G.ch.as<uint32_t>();
     const size_t nbw = (size_t)(Vg + 31) / 32;
     double *d_mu = reinterpret_cast<double *>(reinterpret_cast<char *>(chbm) + ((nbw * 4 + 7) / 8) * 8);
     int32_t *d_cnt = reinterpret_cast<int32_t *>(d_mu + 1);
-    exact_mean(ctx, G.c.as<double>(), Vg, nullptr, d_mu, nullptr);
-    HM_CUDA(cudaMemsetAsync(d_cnt, 0, 4, s));
-    k_cc_bitmap<<<grid_for((int64_t)Vg, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(G.c.as<double>(), d_mu, chbm,
-                                                                                    d_cnt, Vg);
-    check_launch("k_cc_bitmap");
-    count_launch(ctx);
+    Buf acc((size_t)EXACT_NLIMB * 8, s);
+    HM_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes, s));
+    int64_t nb = grid_for(Vg, TB, (int64_t)ctx->num_sms * 16);
+    const int64_t need = ((int64_t)Vg + EXACT_MAX_PER_BLOCK - 1) / EXACT_MAX_PER_BLOCK;
+    if (nb < need) nb = need;
+    // finalize + the exact sum of c in one pass; then mu and the CC-node bitmap in one pass
+    k_finalize<<<(unsigned)nb, TB, 0, s>>>(
+        o2n, label, csize, G.row_ptr.as<int32_t>(), S_rel, scalars, S_orig, G.S.as<uint64_t>(), G.k.as<int32_t>(),
+        G.c.as<double>(), G.pen.as<uint64_t>(), G.deg.as<int32_t>(), Vg, voff, acc.as<unsigned long long>(), d_cnt);
+    check_launch("k_finalize");
+    k_mu_bitmap<<<grid_for((int64_t)Vg, TB, (int64_t)ctx->num_sms * 8), TB, 0, s>>>(
+        acc.as<unsigned long long>(), G.c.as<double>(), chbm, d_mu, d_cnt, Vg);
+    check_launch("k_mu_bitmap");
+    count_launch(ctx, 2);
     G.has_results = true;
 }
 
