@@ -167,6 +167,8 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_param("bfs_words", args.words)
     ctx.set_param("bfs_hints", args.hints)
     ctx.set_param("timing", 1)
+    if args.fused or args.separate:
+        ctx.set_param("bfs_fuse", 1 if args.fused else 0)
     for kv in args.set:                      # extra library parameters (A/B experiments)
         k, v = kv.split("=")
         ctx.set_param(k, int(v))
@@ -218,11 +220,10 @@ def run_ours(args, rank, world, local_rank):
                     dist.all_reduce(S_all[:len(gids) * V], op=dist.ReduceOp.SUM)
             for k, g in enumerate(gids):
                 ctx.closeness_combine(g, S_all[k * V:(k + 1) * V])
-        elif args.fused:
-            ctx.closeness_multi(list(gids))
         else:
-            for g in gids:
-                ctx.closeness(g, out={})
+            # every graph of the step in one call: the library fuses them into one MS-BFS pass when
+            # they are too small to fill the GPU alone (bfs_fuse 2; --fused forces 1, --separate 0)
+            ctx.closeness_multi(list(gids))
 
     def hot_step():
         ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
@@ -252,6 +253,8 @@ def run_ours(args, rank, world, local_rank):
     ctx.sync()
     probe = ctx.stats(reset=True)
     launches_per_step = probe["launches"]
+    n_graphs_step = len(h.layers) + len(h.subsets)
+    fused_step = probe["bfs_launches"] < n_graphs_step          # the library fused the step's graphs
     graph_info["host_syncs_per_step"] = probe["host_syncs"]
     if args.graph and not args.shard and probe["host_syncs"] == 0:
         try:
@@ -309,7 +312,7 @@ def run_ours(args, rank, world, local_rank):
     # SURVEY §8(d) / PAPER.md:373 accounting: Psi per layer, AND, ground-truth closeness, Theta (CC1, CC2)
     breakdown = None
     accuracy = None
-    if not args.shard and not args.fused:
+    if not args.shard:
         ev = []
 
         def mark(name):
@@ -411,7 +414,7 @@ def run_ours(args, rank, world, local_rank):
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     traffic, traffic_src = measured_traffic(args)
     per_graph = {}
-    if not args.shard and not args.fused:
+    if not args.shard:
         ctx.sync()
         ctx.stats(reset=True)
         gl = [(f"L{i}", i) for i in range(len(h.layers))]
@@ -441,7 +444,32 @@ def run_ours(args, rank, world, local_rank):
             per_graph[name] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
         for g in ands:
             ctx.free_graph(g)
-    if per_graph:                           # per-launch numbers from the eager per-graph pass
+    step_fused = None
+    if fused_step and not args.shard:
+        # the step's own fused MS-BFS launch (one eager Psi over all graphs of the step)
+        ctx.sync()
+        ctx.stats(reset=True)
+        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        flush_l2()
+        psi(list(range(len(h.layers))) + ands)
+        ctx.sync()
+        sg = ctx.stats(reset=True)
+        t = sg["bfs_ms"] / 1e3
+        model = sg["bfs_model_bytes"]
+        comp = sg["bfs_state_bytes"] + sg["bfs_csr_bytes"]
+        step_fused = {"graphs": n_graphs_step, "launches": sg["bfs_launches"], "ms": round(sg["bfs_ms"], 4),
+                      "levels": sg["bfs_levels"], "batches": sg["bfs_batches"], "model_bytes": model,
+                      "compulsory_bytes": comp, "row_commits": sg["bfs_row_commits"],
+                      "model_frac": round(model / t / 1e9 / peak_gbs, 4) if t > 0 else None,
+                      "compulsory_frac": round(comp / t / 1e9 / peak_gbs, 4) if t > 0 else None}
+        for g in ands:
+            ctx.free_graph(g)
+    if step_fused:                          # headline: the fused launch the step runs
+        n_bfs = step_fused["launches"]
+        bfs_ms_avg = step_fused["ms"] / max(1, n_bfs)
+        levels_per_launch = step_fused["levels"] / max(1, n_bfs)
+        bfs_ms_step = step_fused["ms"]
+    elif per_graph:                         # per-launch numbers from the eager per-graph pass
         n_bfs = len(per_graph)
         bfs_ms_avg = float(np.mean([v["ms"] for v in per_graph.values()]))
         levels_per_launch = float(np.mean([v["levels"] for v in per_graph.values()]))
@@ -455,7 +483,12 @@ def run_ours(args, rank, world, local_rank):
     # C5 step, ~75 % of it); algorithmic bytes = SURVEY §8(d) dense-level model of this algorithm,
     # accumulated by the kernel per batch:  L * (4 (rows + 1) + 4 arcs + 2 R rows),  R = 8 W bytes
     layer_e = [v for k, v in per_graph.items() if k.startswith("L")]
-    if layer_e:
+    if step_fused:
+        dom_ms = step_fused["ms"] / max(1, step_fused["launches"])
+        dom_bytes = step_fused["model_bytes"] / max(1, step_fused["launches"])
+        dom_traffic = None
+        dom_name = "msbfs_kernel, the step's fused launch over all its graphs (bfs_fuse)"
+    elif layer_e:
         dom_ms = float(np.mean([v["ms"] for v in layer_e]))
         dom_bytes = float(np.mean([v["model_bytes"] for v in layer_e]))
         dom_traffic = (float(np.mean([v["ncu_dram_bytes"] for v in layer_e]))
@@ -478,7 +511,7 @@ def run_ours(args, rank, world, local_rank):
                               "ncu_dram = dram__bytes_read+write of the same launch (ncu, serialised, cold cache)",
             "levels_per_launch": levels_per_launch, "bfs_ms_per_launch_all": bfs_ms_avg,
             "bfs_share_of_step": bfs_ms_step / max(ms_per_step, 1e-9),
-            "fused_graphs": 1 if (not args.fused) else len(arcs)}
+            "fused_graphs": n_graphs_step if fused_step else 1, "step_fused_launch": step_fused}
 
     line = {
         "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",
@@ -724,7 +757,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time the eager step even when it could be captured in a CUDA graph")
-    ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step")
+    ap.add_argument("--fused", action="store_true", help="one fused MS-BFS pass over all graphs of the step "
+                    "(bfs_fuse 1; default: the library's automatic choice)")
+    ap.add_argument("--separate", action="store_true", help="one MS-BFS pass per graph (bfs_fuse 0)")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: split every graph's source batches over the ranks, NCCL all-reduce of S")
     ap.add_argument("--no-cpu-baseline", action="store_true")

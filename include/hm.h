@@ -87,6 +87,11 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   the frontier (rows changed at the previous level) marks its neighbours as candidates,
  *                   then only candidate rows pull -- when frontier rows * bfs_td <= the batch's rows, else
  *                   bottom-up over every row not yet complete; 0 = always bottom-up
+ *   "bfs_fuse"    : hm_closeness_multi: 0 one pass per graph, 1 one fused pass over the disjoint union,
+ *                   2 (default) fused when sum of V <= 2^17 (graphs too small to fill the GPU alone)
+ *   "topk_tiles"  : top-K lists (K <= 4096, n > 4096): 1 (default) one launch -- per-tile block-local radix
+ *                   selects, then the last tile merges and sorts -- where the G = ceil(n / 8192) tiles' K
+ *                   candidates fit one block (G * K <= 16384), 0 the cooperative 12-pass radix select
  *   "bfs_chg_smem": 1 stages the per-level change bitmaps in shared memory, 0 (default) reads them via L1
  *   "timing"      : 1 = record CUDA events around the MS-BFS kernel, 2 = also around every phase of
  *                   closeness / compose / top-K / aggregation (see hm_get_stats)
@@ -149,14 +154,16 @@ hm_status hm_free_graph(hm_ctx *ctx, int32_t g);
 hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reach,
                        double *closeness, uint64_t *pen_sum);
 
-/* hm_closeness for n >= 1 distinct graphs in ONE fused pass: the graphs are
- * independent problems (the layers of a HoMLN, analysed "in parallel",
- * PAPER.md:142, plus any aggregate), so their all-sources BFS runs over the
- * disjoint union and shares every level step.  Results are per graph,
- * identical to n separate hm_closeness calls, cached for hm_compose /
- * hm_topk_closeness / hm_cc_nodes and readable with hm_closeness_results.
- * graph_ids: host array.  Errors: n < 1 or repeated id -> EINVAL; unknown id
- * -> ESTATE; sum of V >= 2^26 -> ERANGE. */
+/* hm_closeness for n >= 1 distinct graphs: the graphs are independent problems
+ * (the layers of a HoMLN, analysed "in parallel", plus any
+ * aggregate).  Fused ("bfs_fuse" 1, or 2 = default when sum of V <= 2^17):
+ * their all-sources BFS runs over the disjoint union in ONE pass and shares
+ * every level step (no pruning, no host round trip); otherwise one hm_closeness
+ * pass per graph.  Results are per graph, identical to n separate hm_closeness
+ * calls either way, cached for hm_compose / hm_topk_closeness / hm_cc_nodes and
+ * readable with hm_closeness_results.  graph_ids: host array.  Errors: n < 1 or
+ * repeated id -> EINVAL; unknown id -> ESTATE; fused with n > 64 -> EINVAL;
+ * fused with sum of V >= 2^26 -> ERANGE. */
 hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n);
 
 /* Sharded Psi (source batches split over GPUs, one sum

@@ -292,10 +292,13 @@ __global__ void k_perm(const uint32_t *rk, const uint32_t *olds, const int32_t *
     if (blockIdx.x == 0 && threadIdx.x == 0) new_deg[V] = 0;
 }
 
+// rows of more than RELABEL_BIG arcs (R-MAT hubs of 5-8 K arcs) would hold one warp for hundreds of
+// dependent-load rounds: they are listed (scalars[15] counts them) and relabelled by k_relabel_big
+constexpr int RELABEL_BIG = 1024;
 __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const int32_t *__restrict__ nrp, const int32_t *__restrict__ new_to_old,
                                const int32_t *__restrict__ old_to_new, int32_t *__restrict__ ncol,
-                               int32_t *heavy, int32_t *scalars, const int32_t *rem, int V) {
+                               int32_t *heavy, int32_t *scalars, const int32_t *rem, int V, int32_t *big) {
     const int lane = threadIdx.x & 31;
     const int heavy_deg = scalars[4];
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -304,6 +307,10 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
     for (int64_t i = w0; i < n_live; i += nw) {
         const int old = new_to_old[i];
         const int rb = row_ptr[old], re = row_ptr[old + 1];
+        if (big && re - rb > RELABEL_BIG) {                 // hub row: a whole block (k_relabel_big)
+            if (lane == 0) big[atomicAdd(scalars + 15, 1)] = (int)i;
+            continue;
+        }
         const int ob = nrp[i];
         // packed arc: (relabelled neighbour << 5) | (row index within its 32-row group);
         // with pruning only arcs to live (unpeeled) neighbours, order kept
@@ -317,6 +324,53 @@ __global__ void k_relabel_cols(const int32_t *__restrict__ row_ptr, const int32_
             outn += __popc(b);
         }
         if (lane == 0 && outn > heavy_deg) heavy[atomicAdd(scalars + 3, 1)] = (int)i;
+    }
+}
+
+// the listed hub rows, a block per row: 1024 arcs per round, kept positions (pruning drops arcs to
+// peeled vertices, order kept) from a block-wide ballot scan
+__global__ void __launch_bounds__(1024) k_relabel_big(const int32_t *__restrict__ row_ptr,
+                                                      const int32_t *__restrict__ col, const int32_t *__restrict__ nrp,
+                                                      const int32_t *__restrict__ new_to_old,
+                                                      const int32_t *__restrict__ old_to_new, int32_t *__restrict__ ncol,
+                                                      int32_t *heavy, int32_t *scalars, const int32_t *rem,
+                                                      const int32_t *big) {
+    __shared__ int s_w[32];
+    __shared__ int s_tot;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int heavy_deg = scalars[4];
+    const int nbig = scalars[15];
+    for (int b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const int i = big[b];
+        const int old = new_to_old[i];
+        const int rb = row_ptr[old], re = row_ptr[old + 1];
+        const int ob = nrp[i];
+        int outn = 0;
+        for (int j0 = rb; j0 < re; j0 += 1024) {
+            const int j = j0 + threadIdx.x;
+            const int u = j < re ? col[j] : 0;
+            const bool keep = j < re && !(rem && rem[u]);
+            const int val = keep ? ((old_to_new[u] << 5) | (i & 31)) : 0;
+            const unsigned bm = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) s_w[wib] = __popc(bm);
+            __syncthreads();
+            if (wib == 0) {
+                const int x = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+                int incl = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                s_w[lane] = incl - x;
+                if (lane == 31) s_tot = incl;
+            }
+            __syncthreads();
+            if (keep) ncol[ob + outn + s_w[wib] + __popc(bm & ((1u << lane) - 1u))] = val;
+            outn += s_tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0 && outn > heavy_deg) heavy[atomicAdd(scalars + 3, 1)] = i;
     }
 }
 
@@ -362,8 +416,19 @@ __global__ void k_row_T(const int32_t *new_to_old, const uint32_t *tsz, const in
 }
 
 // union CSR of several graphs: graph g's vertex v becomes voff + v
-__global__ void k_union_copy(const int32_t *__restrict__ rp, const int32_t *__restrict__ col, int V, int64_t nnz,
-                             int voff, int64_t aoff, int32_t *rp_u, int32_t *col_u) {
+// graph i of a fused union: its arcs start after the exact arc counts of graphs 0..i-1, read on the
+// device (an AND graph's count lives only in its row_ptr[V]), so building the union needs no host
+// round trip
+constexpr int UNION_MAX = 64;
+struct UnionEnds {
+    const int32_t *end[UNION_MAX];   // &row_ptr_j[V_j] of the graphs before this one
+    int n;
+};
+__global__ void k_union_copy(const int32_t *__restrict__ rp, const int32_t *__restrict__ col, int V, UnionEnds pre,
+                             int voff, int32_t *rp_u, int32_t *col_u) {
+    int64_t aoff = 0;
+    for (int k = 0; k < pre.n; ++k) aoff += *pre.end[k];
+    const int64_t nnz = rp[V];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= V; i += (int64_t)gridDim.x * blockDim.x)
         rp_u[voff + i] = (int32_t)(rp[i] + aoff);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
@@ -740,6 +805,24 @@ static void finalize_graph(hm_ctx *ctx, Graph &G, const int32_t *o2n, const int3
 
 void closeness(hm_ctx *ctx, Graph &G) { closeness_multi(ctx, std::vector<Graph *>{&G}); }
 
+// Fusing pays while the graphs are too small to fill the GPU one at a time (C2, 4 graphs of 16 K
+// vertices: 3.24 -> 1.77 ms per step; C1, 3 graphs of 1000 vertices: 0.55 ms with three one-CTA
+// small-path passes, 0.42 ms fused); larger graphs each fill the grid, keep their own pruning (the
+// fused pass does not prune) and their state rows stay L2-resident (C3, 14 graphs of 64 K vertices:
+// 41.1 ms separately, 57.8 ms fused).
+constexpr int64_t FUSE_AUTO_MAX_V = (int64_t)1 << 17;
+void closeness_group(hm_ctx *ctx, const std::vector<Graph *> &gs) {
+    int64_t Vs = 0;
+    for (const Graph *g : gs) Vs += g->V;
+    const int f = ctx->params.bfs_fuse;
+    const bool fuse = gs.size() > 1 && (f == 1 || (f == 2 && Vs <= FUSE_AUTO_MAX_V));
+    if (fuse) {
+        closeness_multi(ctx, gs);
+        return;
+    }
+    for (Graph *g : gs) closeness_multi(ctx, std::vector<Graph *>{g});
+}
+
 void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out) {
     closeness_multi(ctx, std::vector<Graph *>{&G}, shard, nshards, d_S_out, nullptr);
 }
@@ -765,8 +848,9 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     int64_t Vu64 = 0, nnz_u = 0;
     for (Graph *g : gs) {
         Vu64 += g->V;
-        // the union CSR concatenates arcs: exact counts (an AND graph's may still be an upper bound)
-        nnz_u += gs.size() > 1 ? exact_nnz(ctx, *g) : g->nnz;
+        // the union CSR concatenates arcs: sized by the host counts (an AND graph's is an upper bound;
+        // the exact offsets are taken on the device, k_union_copy)
+        nnz_u += g->nnz;
     }
     HM_REQUIRE(Vu64 < (1 << 26), HM_ERANGE, "hm_closeness supports sum V < 2^26 (packed arc format)");
     HM_REQUIRE(nnz_u < (int64_t)INT32_MAX, HM_ERANGE, "union of graphs too large for an int32 CSR");
@@ -797,16 +881,18 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     if (gs.size() > 1) {
         rp_ub.alloc((size_t)(V + 1) * 4, s);
         col_ub.alloc((size_t)(nnz_u > 0 ? nnz_u : 1) * 4, s);
+        HM_REQUIRE(gs.size() <= (size_t)UNION_MAX, HM_EINVAL, "hm_closeness_multi fuses at most 64 graphs");
         int vo = 0;
-        int64_t ao = 0;
+        UnionEnds pre{};
         for (size_t i = 0; i < gs.size(); ++i) {
             voff[i] = vo;
             const int64_t n = (int64_t)gs[i]->V + 1 > gs[i]->nnz ? (int64_t)gs[i]->V + 1 : gs[i]->nnz;
+            pre.n = (int)i;
             k_union_copy<<<grid_for(n, TB, (int64_t)ctx->num_sms * 16), TB, 0, s>>>(
-                gs[i]->row_ptr.as<int32_t>(), gs[i]->col.as<int32_t>(), gs[i]->V, gs[i]->nnz, vo, ao,
+                gs[i]->row_ptr.as<int32_t>(), gs[i]->col.as<int32_t>(), gs[i]->V, pre, vo,
                 rp_ub.as<int32_t>(), col_ub.as<int32_t>());
+            pre.end[i] = gs[i]->row_ptr.as<int32_t>() + gs[i]->V;
             vo += gs[i]->V;
-            ao += gs[i]->nnz;
         }
         check_launch("k_union_copy");
         count_launch(ctx, (int)gs.size());
@@ -975,11 +1061,28 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // sparser ones, where a row of a few dozen arcs already stalls its warp's lock-step rounds
     // (heavy sweep over C2-C4 layers and AND graphs)
     k_heavy_threshold<<<1, 32, 0, s>>>(U.rp, V, heavy_param, scalars);
-    k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
-                                     n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
-                                     heavy.as<int32_t>(), scalars, rem, V);
-    check_launch("k_relabel_cols");
-    count_launch(ctx, 2);
+    {
+        // hub rows to k_relabel_big -- unless the graph's cached shape says it has none
+        const PruneDecision *pdh = gs.size() == 1 ? (gs[0]->and_key.empty() ? &gs[0]->pdec
+                                                      : (ctx->and_pdec.count(gs[0]->and_key)
+                                                             ? &ctx->and_pdec[gs[0]->and_key] : nullptr))
+                                                   : nullptr;
+        const bool may_big = !(pdh && pdh->valid && pdh->maxdeg <= RELABEL_BIG);
+        Buf bigl;
+        if (may_big) bigl.alloc((size_t)(U.nnz / RELABEL_BIG + 1) * 4, s);
+        k_relabel_cols<<<gw, TB, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(),
+                                         n2o.as<int32_t>(), o2n.as<int32_t>(), ncol.as<int32_t>(),
+                                         heavy.as<int32_t>(), scalars, rem, V, may_big ? bigl.as<int32_t>() : nullptr);
+        check_launch("k_relabel_cols");
+        count_launch(ctx, 2);
+        if (may_big) {
+            k_relabel_big<<<ctx->num_sms, 1024, 0, s>>>(U.rp, U.col, nrp.as<int32_t>(), n2o.as<int32_t>(),
+                                                       o2n.as<int32_t>(), ncol.as<int32_t>(), heavy.as<int32_t>(),
+                                                       scalars, rem, bigl.as<int32_t>());
+            check_launch("k_relabel_big");
+            count_launch(ctx);
+        }
+    }
     phase_end(ctx, PH_RELABEL, ph);
     ph = phase_begin(ctx);
 
@@ -1087,6 +1190,21 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     }
     a.F[0] = F0.as<uint64_t>();
     a.F[1] = F1.as<uint64_t>();
+    // segment skipping (bfs_meta): per-row segment masks, double-buffered like F; built for the default
+    // kernels (W = 64 with 16-lane teams and 4 gathers in flight, W = 128 with 2)
+    Buf metab;
+    a.meta[0] = a.meta[1] = nullptr;
+    {
+        const int tl = ctx->params.bfs_team == 0 ? 16 : ctx->params.bfs_team;
+        const int gd = ctx->params.bfs_gd;
+        const bool two = ctx->params.bfs_blocks_per_sm != 1;
+        const bool built = two && tl == 16 && ((W == 64 && (gd == 0 || gd == 4)) || (W == 128 && (gd == 0 || gd == 2)));
+        if (ctx->params.bfs_meta && built) {
+            metab.alloc((size_t)frows * 8, s);
+            a.meta[0] = metab.as<uint32_t>();
+            a.meta[1] = a.meta[0] + frows;
+        }
+    }
     uint32_t *bm = bms.as<uint32_t>();
     for (int i = 0; i < 3; ++i) a.chg[i] = bm + i * bmw;
     a.done = bm + 3 * bmw;

@@ -114,6 +114,10 @@ struct Params {
     int bfs_unit = 0;          // MS-BFS light-path rows per work unit (0 = auto by rows per warp; 32 ... 2)
     int bfs_gd = 0;            // MS-BFS gathers in flight per lane (0 = default)
     int bfs_team = 0;          // MS-BFS lanes per light state row (0 = default)      // stage the change bitmaps in shared memory each level
+    int bfs_fuse = 2;          // hm_closeness_multi: 0 one pass per graph, 1 one fused pass, 2 (auto) fused when
+                               // sum of V <= 2^17 (small graphs that cannot fill the GPU alone)
+    int bfs_meta = 0;          // MS-BFS segment skipping (per-row masks of zero / full segments); 0 off
+    int topk_tiles = 1;        // top-K: 1 two-phase tile select (one launch) where it fits, 0 cooperative radix select
     int bfs_td = 0;            // direction switch: top-down levels when frontier * bfs_td <= rows (0 = off)
     int timing = 0;
     int bfs_dbg = 0;
@@ -214,6 +218,8 @@ void closeness(hm_ctx *ctx, Graph &G);
 void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard = 0, int nshards = 1,
                      uint64_t *d_S_partial = nullptr, const uint64_t *d_S_total = nullptr);
 void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out);
+// hm_closeness_multi: one fused pass or one pass per graph (Params::bfs_fuse)
+void closeness_group(hm_ctx *ctx, const std::vector<Graph *> &gs);
 
 // exact 2-core pruning of the largest component (prune.cu)
 struct Prune {

@@ -137,6 +137,13 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_prune") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_prune must be 0, 1 or 2 (auto)");
         ctx->params.bfs_prune = (int)value;
+    } else if (n == "bfs_meta") {
+        ctx->params.bfs_meta = value ? 1 : 0;
+    } else if (n == "topk_tiles") {
+        ctx->params.topk_tiles = value ? 1 : 0;
+    } else if (n == "bfs_fuse") {
+        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_fuse must be 0, 1 or 2 (auto)");
+        ctx->params.bfs_fuse = (int)value;
     } else if (n == "cc_init") {
         HM_REQUIRE(value >= 0 && value <= 4, HM_EINVAL, "cc_init must be 0, 1, 2, 3 or 4 (auto)");
         ctx->params.cc_init = (int)value;
@@ -290,7 +297,7 @@ hm_status hm_closeness_multi(hm_ctx *ctx, const int32_t *graph_ids, int32_t n) {
     HM_REQUIRE((int32_t)seen.size() == n, HM_EINVAL, "repeated graph id");
     std::vector<Graph *> gs;
     for (int i = 0; i < n; ++i) gs.push_back(&graph(ctx, graph_ids[i]));
-    closeness_multi(ctx, gs);
+    closeness_group(ctx, gs);
     HM_API_END(ctx)
 }
 

@@ -37,9 +37,21 @@ namespace {
 constexpr int TB = 256;
 
 // P = the largest component (ties: smallest root); key = size << 32 | (V - 1 - root)
+// (warp max first: graphs with many isolated vertices have as many roots, and one global atomicMax
+// per root serialises on `best`)
 __global__ void k_pick_largest(const int32_t *label, const int32_t *csize, unsigned long long *best, int V) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-        if (label[v] == v) atomicMax(best, ((unsigned long long)csize[v] << 32) | (unsigned)(V - 1 - v));
+    const int stride = gridDim.x * blockDim.x;
+    for (int v0 = blockIdx.x * blockDim.x; v0 < V; v0 += stride) {      // warp-uniform trip count
+        const int v = v0 + threadIdx.x;
+        unsigned long long k = 0ull;
+        if (v < V && label[v] == v) k = ((unsigned long long)csize[v] << 32) | (unsigned)(V - 1 - v);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, k, o);
+            k = y > k ? y : k;
+        }
+        if ((threadIdx.x & 31) == 0 && k) atomicMax(best, k);
+    }
 }
 
 __device__ __forceinline__ int live_neighbour(const int32_t *rp, const int32_t *col, const int32_t *rem, int v,
@@ -110,20 +122,31 @@ __global__ void k_prune_stats(const int32_t *label, const int32_t *csize, const 
                               const unsigned long long *best, int32_t *lsize, unsigned long long *Cc,
                               const unsigned long long *tD, int32_t *stats, int V) {
     const int P = V - 1 - (int)(*best & 0xffffffffull);
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
-        const int l = label[v];
-        if (rem[v] == 0) {
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * blockDim.x;
+    for (int v0 = blockIdx.x * blockDim.x; v0 < V; v0 += stride) {      // warp-uniform trip count
+        const int v = v0 + threadIdx.x;
+        const bool in = v < V;
+        const int l = in ? label[v] : -1;
+        const bool live = in && rem[v] == 0;
+        if (live) {
             const unsigned act = __activemask();
             const unsigned same = __match_any_sync(act, l);                 // warp-aggregated count
-            if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(lsize + l, __popc(same));
-            if (l == P) {
-                const unsigned actp = __activemask();
-                const unsigned tmax = __reduce_max_sync(actp, tsz[v] - 1u);   // warp-aggregated max T
-                if ((threadIdx.x & 31) == __ffs(actp) - 1) atomicMax(stats + 2, (int)tmax);
-                if (tD[v]) atomicAdd(Cc + l, tD[v]);          // (1): the component constant
-            }
+            if (lane == __ffs(same) - 1) atomicAdd(lsize + l, __popc(same));
         }
-        if (l == v && v != P) atomicMax(stats + 1, csize[v]);
+        // warp-aggregated: max T over P's core, (1) the component constant of P, the largest other root
+        const bool inP = live && l == P;
+        const unsigned tmax = __reduce_max_sync(0xffffffffu, inP ? tsz[v] - 1u : 0u);
+        unsigned long long td = inP ? tD[v] : 0ull;
+        const unsigned omax = __reduce_max_sync(0xffffffffu, (in && l == v && v != P) ? (unsigned)csize[v] : 0u);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) td += __shfl_xor_sync(0xffffffffu, td, o);
+        const bool anyP = __any_sync(0xffffffffu, inP);
+        if (lane == 0) {
+            if (anyP) atomicMax(stats + 2, (int)tmax);
+            if (td) atomicAdd(Cc + P, td);
+            if (omax) atomicMax(stats + 1, (int)omax);
+        }
     }
 }
 

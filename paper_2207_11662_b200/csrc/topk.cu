@@ -231,6 +231,190 @@ __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t *ok, const u
     for (int i = threadIdx.x; i < K; i += blockDim.x) out[i] = (int32_t)si[i];
 }
 
+// ---- two-phase tile select (n > SORT_MAX, K <= SORT_MAX): no grid barrier.
+// Phase A: block b selects the K smallest of its TILE_E pairs in shared memory (a block-local radix
+// select, stopping at the first digit whose bin is taken whole) and writes them, padded to K with the
+// sentinel (~0, ~0) that exceeds every real pair, to its candidate slot.  Phase B: the last block to
+// finish (ticket) selects the K smallest of the G*K candidates the same way, sorts them (bitonic) and
+// writes their ids.  One launch instead of a 12-pass cooperative select (C3: 40 top-K lists per step).
+constexpr int TT = 1024;            // threads per block
+constexpr int TILE_E = 8192;        // pairs per phase-A block
+constexpr int CAND_MAX = 16384;     // candidates phase B holds in shared memory (G * K)
+
+__device__ __forceinline__ bool le_depth(uint64_t k, uint32_t id, uint64_t tk, uint32_t ti, int p) {
+    // the first p + 1 digits of (k, id) <= those of (tk, ti)
+    if (p < 8) {
+        const int sh = 8 * (7 - p);
+        return (k >> sh) <= (tk >> sh);
+    }
+    if (k != tk) return k < tk;
+    const int sh = 8 * (11 - p);
+    return (id >> sh) <= (ti >> sh);
+}
+
+struct BlkSel {
+    unsigned hist[256];
+    unsigned long long pkey;
+    unsigned pid;
+    int rem, pend, cnt;
+};
+
+// block radix select over n pairs in shared memory: afterwards exactly K pairs satisfy
+// le_depth(x, (bs.pkey, bs.pid), bs.pend)
+__device__ void block_select(const uint64_t *sk, const uint32_t *si, int n, int K, BlkSel &bs) {
+    if (threadIdx.x == 0) {
+        bs.pkey = 0ull;
+        bs.pid = 0u;
+        bs.rem = K;
+        bs.pend = -1;
+    }
+    for (int p = 0; p < 12; ++p) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) bs.hist[i] = 0u;
+        __syncthreads();
+        const uint64_t pk = bs.pkey;
+        const uint32_t pi = bs.pid;
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            if (prefix_match(sk[i], si[i], pk, pi, p)) atomicAdd(&bs.hist[digit_of(sk[i], si[i], p)], 1u);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = bs.hist[lane * 8 + q];
+                tot += c[q];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int rem = bs.rem;
+            const unsigned excl = incl - tot;
+            if ((int)excl < rem && rem <= (int)incl) {           // exactly one lane (K <= n)
+                int r = rem - (int)excl, b = 0;
+                for (; b < 7; ++b) {
+                    if (r <= (int)c[b]) break;
+                    r -= (int)c[b];
+                }
+                const unsigned dg = (unsigned)(lane * 8 + b);
+                if (p < 8) bs.pkey |= (unsigned long long)dg << (8 * (7 - p));
+                else bs.pid |= dg << (8 * (11 - p));
+                bs.rem = r;
+                if (r == (int)c[b]) bs.pend = p;                  // the whole bin is taken: done
+            }
+        }
+        __syncthreads();
+        if (bs.pend >= 0) break;                                  // block-uniform
+    }
+}
+
+// the first K pairs of (sk, si) -- P >= K a power of two, slots [K, P) padded by the caller -- sorted
+__device__ void block_bitonic(uint64_t *sk, uint32_t *si, int P) {
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool sw = up ? less_kv(sk[j], si[j], sk[i], si[i]) : less_kv(sk[i], si[i], sk[j], si[j]);
+                    if (sw) {
+                        const uint64_t tk = sk[i]; sk[i] = sk[j]; sk[j] = tk;
+                        const uint32_t ti = si[i]; si[i] = si[j]; si[j] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// selected pairs of (sk, si)[0, n) -> (ok, oi) at positions from the block counter bs.cnt (unordered)
+__device__ void block_compact(const uint64_t *sk, const uint32_t *si, int n, const BlkSel &bs, uint64_t *ok,
+                              uint32_t *oi, int *cnt) {
+    const uint64_t tk = bs.pkey;
+    const uint32_t ti = bs.pid;
+    const int pe = bs.pend;
+    const int lane = threadIdx.x & 31;
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {                 // block-uniform trip count
+        const int i = i0 + threadIdx.x;
+        const bool sel = i < n && le_depth(sk[i], si[i], tk, ti, pe);
+        const unsigned b = __ballot_sync(0xffffffffu, sel);
+        int base = 0;
+        if (lane == 0 && b) base = atomicAdd(cnt, __popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sel) {
+            const int pos = base + __popc(b & ((1u << lane) - 1u));
+            ok[pos] = sk[i];
+            oi[pos] = si[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TT) k_topk_tiles(const uint64_t *__restrict__ keys, int n, int K,
+                                                  uint64_t *cand_k, uint32_t *cand_i, unsigned *ticket,
+                                                  int32_t *out) {
+    extern __shared__ unsigned char smem[];
+    __shared__ BlkSel bs;
+    __shared__ int s_last;
+    const int G = gridDim.x;
+    const int nsm = max(min(n, TILE_E), G * K);                  // pairs the shared arrays hold
+    uint64_t *sk = reinterpret_cast<uint64_t *>(smem);
+    uint32_t *si = reinterpret_cast<uint32_t *>(sk + nsm);
+    // phase A: this block's tile
+    const int i0 = blockIdx.x * TILE_E;
+    const int nb = min(TILE_E, n - i0);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        sk[i] = keys[i0 + i];
+        si[i] = (uint32_t)(i0 + i);
+    }
+    if (threadIdx.x == 0) bs.cnt = 0;
+    __syncthreads();
+    uint64_t *ck = cand_k + (size_t)blockIdx.x * K;
+    uint32_t *ci = cand_i + (size_t)blockIdx.x * K;
+    if (nb <= K) {
+        for (int i = threadIdx.x; i < K; i += blockDim.x) {
+            ck[i] = i < nb ? sk[i] : ~0ull;
+            ci[i] = i < nb ? si[i] : 0xffffffffu;
+        }
+    } else {
+        block_select(sk, si, nb, K, bs);
+        block_compact(sk, si, nb, bs, ck, ci, &bs.cnt);          // exactly K
+    }
+    // the last block to finish merges
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == (unsigned)(G - 1)) ? 1 : 0;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int nc = G * K;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+        sk[i] = __ldcg(cand_k + i);
+        si[i] = __ldcg(cand_i + i);
+    }
+    if (threadIdx.x == 0) bs.cnt = 0;
+    __syncthreads();
+    block_select(sk, si, nc, K, bs);
+    // the K selected to the front of the candidate buffer (block 0's slot is re-read below)
+    uint64_t *rk = cand_k + nc;
+    uint32_t *ri = cand_i + nc;
+    block_compact(sk, si, nc, bs, rk, ri, &bs.cnt);
+    __threadfence_block();
+    __syncthreads();
+    int P = 1;
+    while (P < K) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        sk[i] = i < K ? __ldcg(rk + i) : ~0ull;
+        si[i] = i < K ? __ldcg(ri + i) : 0xffffffffu;
+    }
+    __syncthreads();
+    block_bitonic(sk, si, P);
+    for (int i = threadIdx.x; i < K; i += blockDim.x) out[i] = (int32_t)si[i];
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
 __global__ void k_iota_u32(uint32_t *p, int n) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = (uint32_t)i;
 }
@@ -278,6 +462,24 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
         check_launch("topk small");
         count_launch(ctx, 1);
         return;
+    }
+    {
+        // two-phase tile select: one launch, no grid barrier (see k_topk_tiles)
+        const int G = (int)((n + TILE_E - 1) / TILE_E);
+        if (ctx->params.topk_tiles && (int64_t)G * K <= CAND_MAX && G <= ctx->num_sms) {
+            const int nsm = (n < TILE_E ? n : TILE_E) > G * K ? (n < TILE_E ? n : TILE_E) : G * K;
+            const size_t sm = (size_t)nsm * 12;
+            Buf cb((size_t)(G + 1) * K * 12 + 16, s);
+            uint64_t *ck = cb.as<uint64_t>();
+            uint32_t *ci = reinterpret_cast<uint32_t *>(ck + (size_t)(G + 1) * K);
+            unsigned *ticket = reinterpret_cast<unsigned *>(ci + (size_t)(G + 1) * K);
+            HM_CUDA(cudaMemsetAsync(ticket, 0, 4, s));
+            HM_CUDA(cudaFuncSetAttribute(k_topk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_topk_tiles<<<G, TT, sm, s>>>(d_keys, n, K, ck, ci, ticket, d_ids_out);
+            check_launch("k_topk_tiles");
+            count_launch(ctx, 1);
+            return;
+        }
     }
     Buf stb(sizeof(SelState), s), ok((size_t)K * 8, s), oid((size_t)K * 4, s);
     SelState *st = stb.as<SelState>();

@@ -1,7 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, EVERY output, in the launch
 configuration bench.py times (library defaults: 4096 sources per batch, 16-lane
 row teams, L2 policy hints, interleaved work units, 2-core pruning; layers
-loaded from device tensors; one hm_closeness per graph).
+loaded from device tensors; every graph of the step through one hm_closeness_multi
+call, as bench.py's Psi -- plus the fused / separate variants of that call).
 
 Expected values come from tests/golden/fullsize_<C>.json, written by
 tools/oracle_golden.py, which runs ONLY the oracle (oracle/) on the inputs of
@@ -55,7 +56,7 @@ def golden(name):
 
 
 def check_graph(ctx, g, V, want, what):
-    got = ctx.closeness(g)
+    got = ctx.closeness_results(g)                   # cached by the step's hm_closeness_multi
     deg = ctx.degrees(g)
     nodes, cnt, mu = ctx.cc_nodes(g)
     assert cnt == len(nodes) == want["n_CH"], what
@@ -69,13 +70,16 @@ def check_graph(ctx, g, V, want, what):
     return got
 
 
-KNOBS = {"default": {}, "noprune-w32-contig": {"bfs_prune": 0, "bfs_interleave": 0, "bfs_words": 32}}
+KNOBS = {"default": {}, "noprune-w32-contig": {"bfs_prune": 0, "bfs_interleave": 0, "bfs_words": 32},
+         "separate": {"bfs_fuse": 0}, "fused": {"bfs_fuse": 1}}
 
 
 @pytest.mark.parametrize("name,knobs", [("C1", "default"), ("C2", "default"), ("C3", "default"),
                                         ("C4", "default"), ("C5", "default"),
-                                        ("C4", "noprune-w32-contig"), ("C5", "noprune-w32-contig")],
-                         ids=["C1", "C2", "C3", "C4", "C5", "C4-noprune-w32", "C5-noprune-w32"])
+                                        ("C4", "noprune-w32-contig"), ("C5", "noprune-w32-contig"),
+                                        ("C2", "separate"), ("C3", "fused"), ("C1", "fused")],
+                         ids=["C1", "C2", "C3", "C4", "C5", "C4-noprune-w32", "C5-noprune-w32",
+                              "C2-separate", "C3-fused", "C1-fused"])
 def test_fullsize_config(Context, name, knobs):
     import torch
     gold = golden(name)
@@ -86,12 +90,15 @@ def test_fullsize_config(Context, name, knobs):
         for k, v in KNOBS[knobs].items():
             ctx.set_param(k, v)
         ctx.load_layers(V, [torch.from_numpy(L).cuda() for L in h.layers])
+        # bench's Psi: every layer and AND graph of the step in one hm_closeness_multi call (one fused
+        # pass or one pass per graph, bfs_fuse)
+        ands = [ctx.and_aggregate(want["T"]) for want in gold["ands"]]
+        ctx.closeness_multi(list(range(len(h.layers))) + ands)
         for i in range(len(h.layers)):
             check_graph(ctx, i, V, gold["layers"][i], f"{name} layer {i}")
-        for want in gold["ands"]:
+        for want, g in zip(gold["ands"], ands):
             T = want["T"]
             tag = f"{name} AND{T}"
-            g = ctx.and_aggregate(T)
             rp, col = ctx.graph_csr(g)
             src = np.repeat(np.arange(V, dtype=np.int64), np.diff(rp))
             keep = src < col

@@ -430,6 +430,42 @@ def test_set_metrics_edge_cases(hm):
             ctx.set_metrics(0, [], [])
 
 
+@pytest.mark.parametrize("V", [4097, 8192, 8193, 40000, 300000])
+def test_topk_paths_with_ties(hm, V):
+    """top-K (ties to the lower id, Z14) on tie-heavy closeness vectors, through the
+    one-launch tile select (topk_tiles 1: tiles of 8192, a ragged last tile, candidates G * K up to
+    the 16384 limit) and the cooperative radix select (0): identical lists, equal to the oracle's
+    ranking of the same closeness values.  The graph is many identical 6-cycles (equal closeness),
+    isolated vertices (closeness 0) and a random sparse part."""
+    rng = np.random.default_rng(V)
+    E = set()
+    n_cyc = V // 12
+    for c in range(n_cyc):                              # identical 6-cycles: 6 * n_cyc tied vertices
+        b = 6 * c
+        E |= {(b + i, b + (i + 1) % 6) for i in range(6)}
+    lo = 6 * n_cyc
+    rest = np.arange(lo, V)
+    sparse = rest[: len(rest) // 2]                      # the other half of `rest` stays isolated
+    for _ in range(len(sparse)):
+        a, b = rng.choice(sparse, 2)
+        if a != b:
+            E.add((int(min(a, b)), int(max(a, b))))
+    with hm() as ctx:
+        ctx.load_layers(V, [edges_arr(E)])
+        c = ctx.closeness(0)["c"].tolist()
+        G = (V + 8191) // 8192
+        for K in sorted({1, 2, 7, 100, 1000, 4096, min(V, 16384 // G)}):
+            if K > V or K > 4096:
+                continue
+            want = O.topk_closeness(c, K)
+            got = {}
+            for tiles in (1, 0):
+                ctx.set_param("topk_tiles", tiles)
+                got[tiles] = ctx.topk_closeness(0, K).tolist()
+            assert got[1] == want and got[0] == want, (V, K)
+        ctx.set_param("topk_tiles", 1)
+
+
 def test_device_tensors_roundtrip(hm):
     import torch
     h = build_config("C5", V=2048)
@@ -451,16 +487,26 @@ def test_device_tensors_roundtrip(hm):
         assert ids.cpu().tolist() == O.topk_closeness(res["c"], 10)
 
 
-@pytest.mark.parametrize("name,V", [("C3", 1024), ("C5", 4096), ("C4", 2048)])
-def test_closeness_multi_fused(hm, name, V):
-    """one fused pass over layers + AND graphs == separate passes == oracle."""
+@pytest.mark.parametrize("name,V,fuse", [("C3", 1024, 1), ("C5", 4096, 1), ("C4", 2048, 1), ("C1", 1000, 1),
+                                         ("C2", 4096, 2), ("C1", 1000, 2), ("C5", 2048, 0)])
+def test_closeness_multi_fused(hm, name, V, fuse):
+    """hm_closeness_multi over layers + AND graphs (one fused pass: bfs_fuse 1; automatic: 2; one pass
+    per graph: 0) == separate passes == oracle; the fused pass makes no host round trip."""
     h = build_config(name, V=V)
     Es = [set(map(tuple, L.tolist())) for L in h.layers]
     with hm() as ctx:
+        ctx.set_param("bfs_fuse", fuse)
         ids, _ = ctx.load_layers(h.V, h.layers)
         ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
         gids = list(ids) + ands
+        ctx.sync()
+        ctx.stats(reset=True)
         ctx.closeness_multi(gids)
+        st = ctx.stats(reset=True)
+        fused_expected = len(gids) > 1 and (fuse == 1 or (fuse == 2 and V * len(gids) <= (1 << 17)))
+        assert st["bfs_launches"] == (1 if fused_expected else len(gids))
+        if fused_expected:
+            assert st["host_syncs"] == 0
         fused = {g: ctx.closeness_results(g) for g in gids}
         fused_ch = {g: ctx.cc_nodes(g) for g in gids}
         for g in gids:
