@@ -1190,21 +1190,6 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     }
     a.F[0] = F0.as<uint64_t>();
     a.F[1] = F1.as<uint64_t>();
-    // segment skipping (bfs_meta): per-row segment masks, double-buffered like F; built for the default
-    // kernels (W = 64 with 16-lane teams and 4 gathers in flight, W = 128 with 2)
-    Buf metab;
-    a.meta[0] = a.meta[1] = nullptr;
-    {
-        const int tl = ctx->params.bfs_team == 0 ? 16 : ctx->params.bfs_team;
-        const int gd = ctx->params.bfs_gd;
-        const bool two = ctx->params.bfs_blocks_per_sm != 1;
-        const bool built = two && tl == 16 && ((W == 64 && (gd == 0 || gd == 4)) || (W == 128 && (gd == 0 || gd == 2)));
-        if (ctx->params.bfs_meta && built) {
-            metab.alloc((size_t)frows * 8, s);
-            a.meta[0] = metab.as<uint32_t>();
-            a.meta[1] = a.meta[0] + frows;
-        }
-    }
     uint32_t *bm = bms.as<uint32_t>();
     for (int i = 0; i < 3; ++i) a.chg[i] = bm + i * bmw;
     a.done = bm + 3 * bmw;

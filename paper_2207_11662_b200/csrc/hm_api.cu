@@ -137,8 +137,6 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_prune") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_prune must be 0, 1 or 2 (auto)");
         ctx->params.bfs_prune = (int)value;
-    } else if (n == "bfs_meta") {
-        ctx->params.bfs_meta = value ? 1 : 0;
     } else if (n == "topk_tiles") {
         ctx->params.topk_tiles = value ? 1 : 0;
     } else if (n == "bfs_fuse") {
@@ -480,9 +478,11 @@ hm_status hm_sync(hm_ctx *ctx) {
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(out, HM_EINVAL, "null out");
-    unsigned long long dv[7] = {0, 0, 0, 0, 0, 0, 0};
-    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 56, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long dv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
+    // the MS-BFS level guard (a level deeper than the batch's rows): results since the last reset are wrong
+    HM_REQUIRE(dv[7] == 0, HM_ECUDA, "MS-BFS level guard tripped: a BFS ran deeper than its rows (kernel bug)");
     for (auto &pe : ctx->pending) {
         float ms = 0.f;
         HM_CUDA(cudaEventElapsedTime(&ms, pe.first, pe.second));

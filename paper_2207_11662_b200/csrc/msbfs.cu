@@ -154,58 +154,6 @@ struct Prof {
 #endif
 constexpr int HGD = HM_HEAVY_GD;    // heavy-row gathers in flight per team
 
-// Segment skipping (MT): a state row is 16 segments of CPS = W/32 16-byte chunks (chunk c = words 2c,
-// 2c+1; segment c / CPS).  Per row and buffer a 32-bit mask records which segments of the stored V(v)
-// hold a source (bits 0-15) and which hold every source (bits 16-31).  Readers take zero segments as 0
-// and full ones as all ones without loading them; writers store the mixed segments only.  Early levels
-// (visited sets of a few dozen sources) and late ones (nearly complete rows) then move a fraction of
-// the row bytes.
-template <int CPS>
-__device__ __forceinline__ unsigned compress_bits(unsigned x) {   // bits 0, CPS, 2 CPS, ... packed
-    if constexpr (CPS == 1) {
-        return x;
-    } else if constexpr (CPS == 2) {
-        x &= 0x55555555u;
-        x = (x | (x >> 1)) & 0x33333333u;
-        x = (x | (x >> 2)) & 0x0f0f0f0fu;
-        x = (x | (x >> 4)) & 0x00ff00ffu;
-        return (x | (x >> 8)) & 0x0000ffffu;
-    } else {
-        static_assert(CPS == 4, "segments of 1, 2 or 4 chunks");
-        x &= 0x11111111u;
-        x = (x | (x >> 3)) & 0x03030303u;
-        x = (x | (x >> 6)) & 0x000f000fu;
-        return (x | (x >> 12)) & 0x000000ffu;
-    }
-}
-__device__ __forceinline__ ulonglong2 seg_value(unsigned m, int seg, bool &load) {
-    // the chunk of a segment from its mask: full -> ones, zero -> 0, mixed -> load
-    load = false;
-    if ((m >> (16 + seg)) & 1u) return make_ulonglong2(~0ull, ~0ull);
-    load = (m >> seg) & 1u;
-    return make_ulonglong2(0ull, 0ull);
-}
-
-template <int T, int CPS>
-__device__ __forceinline__ int tl_seg() { return (int)((threadIdx.x & 31) % T) / CPS; }
-
-// segment masks of a row held one 16-byte chunk per lane by the `nl` lanes of `tmask` (from lane tbase,
-// chunk = lane - tbase): (nonzero segments) | (full segments) << 16; `mixed` = this lane's segment is
-// neither (it must be stored).  Every lane of tmask must call it.
-template <int CPS>
-__device__ __forceinline__ unsigned seg_masks(ulonglong2 v, unsigned tmask, int tbase, int nl, bool &mixed) {
-    int z = (v.x | v.y) == 0ull, f = (v.x & v.y) == ~0ull;
-#pragma unroll
-    for (int o = 1; o < CPS; o <<= 1) {
-        z &= __shfl_xor_sync(tmask, z, o);
-        f &= __shfl_xor_sync(tmask, f, o);
-    }
-    mixed = !z && !f;
-    const unsigned lm = nl >= 32 ? 0xffffffffu : ((1u << nl) - 1u);
-    const unsigned bz = (__ballot_sync(tmask, !z) >> tbase) & lm, bf = (__ballot_sync(tmask, f) >> tbase) & lm;
-    return compress_bits<CPS>(bz) | (compress_bits<CPS>(bf) << 16);
-}
-
 template <int NWARP>
 struct Smem {
     int hi;
@@ -354,7 +302,7 @@ __device__ __noinline__ void td_discover(const int32_t *__restrict__ row_ptr, co
 // of each heavy row), claimed from the level's counter hclaim (nullptr: dealt round-robin over the
 // CTAs), each item's arcs split over the CTA's teams of T = W/2 lanes.  A row of several items ORs its partial rows into hacc; the last item to
 // arrive commits.  Returns whether this thread committed a change.
-template <int W, int BLOCK, bool WT, bool MT>
+template <int W, int BLOCK, bool WT>
 __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                          const int2 *__restrict__ cinfo, const int32_t *__restrict__ heavy,
                                          const int32_t *__restrict__ hstart, unsigned long long *hacc, int32_t *hcnt,
@@ -363,11 +311,8 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
                                  int hi, int n_giant, int64_t base, int d, const uint32_t *chp_s,
                                  uint32_t *has, uint32_t *par, const uint64_t *__restrict__ Fc,
                                  const uint64_t *F0, const uint64_t *F1, uint64_t *__restrict__ Fn,
-                                 uint32_t *chn, const uint32_t *cand, const uint32_t *meta_c,
-                                 const uint32_t *meta0, const uint32_t *meta1, uint32_t *meta_n) {
+                                 uint32_t *chn, const uint32_t *cand) {
     constexpr int T = W / 2;
-    constexpr int CPS = W >= 32 ? W / 32 : 1;          // MT: chunks per segment; lane tl holds chunk tl
-    const int sg = tl_seg<T, CPS>();
     constexpr int TPB = BLOCK / T;
     constexpr int64_t B = 64 * W;
     const int lane = threadIdx.x & 31;
@@ -407,38 +352,26 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
             const int j = j0 + tl;
             int u = 0;
             bool c = false;
-            unsigned mu = 0u;
             if (j < re) {
                 u = col[j] >> 5;
                 c = bit_of(chp_s, u);
-                if (MT && c) mu = meta_c[u];
             }
             unsigned m = __ballot_sync(tmask, c) >> tbase;
             while (m) {                                          // HGD neighbour rows in flight
                 int uq[HGD];
-                unsigned mq[HGD];
         #pragma unroll
                 for (int q = 0; q < HGD; ++q) {
                     uq[q] = -1;
-                    mq[q] = 0u;
                     if (m) {
                         const int t0 = __ffs(m) - 1;
                         m &= m - 1;
                         uq[q] = __shfl_sync(tmask, u, tbase + t0);
-                        if constexpr (MT) mq[q] = __shfl_sync(tmask, mu, tbase + t0);
                     }
                 }
                 ulonglong2 x[HGD];
         #pragma unroll
-                for (int q = 0; q < HGD; ++q) {
-                    if constexpr (MT) {
-                        bool ld;
-                        x[q] = seg_value(mq[q], sg, ld);
-                        if (uq[q] >= 0 && ld) x[q] = ld2(Fc + (size_t)uq[q] * W + 2 * tl);
-                    } else {
-                        x[q] = uq[q] >= 0 ? ld2(Fc + (size_t)uq[q] * W + 2 * tl) : make_ulonglong2(0ull, 0ull);
-                    }
-                }
+                for (int q = 0; q < HGD; ++q)
+                    x[q] = uq[q] >= 0 ? ld2(Fc + (size_t)uq[q] * W + 2 * tl) : make_ulonglong2(0ull, 0ull);
         #pragma unroll
                 for (int q = 0; q < HGD; ++q) {
                     acc.x |= x[q].x;
@@ -478,16 +411,7 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
         if (tib == 0) {
             // own visited set V_{d-1}(v): in the buffer of the level that last wrote it
             ulonglong2 vv = make_ulonglong2(0ull, 0ull);
-            if constexpr (MT) {
-                if (bit_of(has, v)) {
-                    const bool pb = bit_of(par, v);
-                    bool ld;
-                    vv = seg_value((pb ? meta1 : meta0)[v], sg, ld);
-                    if (ld) vv = ld2((pb ? F1 : F0) + (size_t)v * W + 2 * tl);
-                }
-            } else {
-                if (bit_of(has, v)) vv = ld2((bit_of(par, v) ? F1 : F0) + (size_t)v * W + 2 * tl);
-            }
+            if (bit_of(has, v)) vv = ld2((bit_of(par, v) ? F1 : F0) + (size_t)v * W + 2 * tl);
             const ulonglong2 nw = make_ulonglong2(acc.x & ~vv.x, acc.y & ~vv.y);
             int cnt = __popcll(nw.x) + __popcll(nw.y);
 #pragma unroll
@@ -502,15 +426,7 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
                 for (int o = T / 2; o > 0; o >>= 1) wsum += __shfl_xor_sync(tmask, wsum, o);
             }
             if (cnt) {
-                const ulonglong2 nv = make_ulonglong2(nw.x | vv.x, nw.y | vv.y);   // V_d(v)
-                if constexpr (MT) {
-                    bool mixed;
-                    const unsigned mn = seg_masks<CPS>(nv, tmask, tbase, T, mixed);
-                    if (mixed) st2(Fn + (size_t)v * W + 2 * tl, nv);
-                    if (tl == 0) meta_n[v] = mn;
-                } else {
-                    st2(Fn + (size_t)v * W + 2 * tl, nv);
-                }
+                st2(Fn + (size_t)v * W + 2 * tl, make_ulonglong2(nw.x | vv.x, nw.y | vv.y));   // V_d(v)
                 if (tl == 0) {
                     const int2 ci = (v < n_giant ? make_int2(0, n_giant) : cinfo[v]);
                     int64_t nb = (int64_t)ci.y - base;
@@ -541,12 +457,8 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
 // WT: weighted sums for the pruned component (prune.cu): S(v) += d * sum over the new
 // sources s of (1 + T(s)), the T sum taken from per-batch bit planes of T in shared memory
 // HV: heavy-row path compiled in (false only for graphs without heavy rows: a leaner kernel)
-// MT: segment skipping (BfsArgs::meta), W >= 32
-template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, bool MT = false,
-          int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
+template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
-    static_assert(!MT || W >= 32, "segment skipping needs rows of >= 16 chunks");
-    constexpr int CPS = W >= 32 ? W / 32 : 1;     // MT: 16-byte chunks per segment
     constexpr int T = W / 2 < 32 ? W / 2 : 32;   // lanes per row in the heavy path (W <= 64 with heavy rows)
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
     constexpr int64_t B = 64 * W;      // sources per batch
@@ -576,8 +488,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     const int tib = threadIdx.x / T;
     const int ltl = lane % TL;
     const int lteam = lane / TL;
-    // LDGSTS ring after the bitmap staging and the MT staging
-    const int ring_off = (a.chg_smem ? (a.chg_words >> 2) : 0) + (MT ? (BLOCK / 32) * CAP / 4 : 0);
+    const int ring_off = a.chg_smem ? (a.chg_words >> 2) : 0;     // LDGSTS ring after the bitmap staging
     (void)ring_off;
 
     const int n_live = a.scalars[0];
@@ -589,8 +500,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     int32_t *su = sm.su[wib];
     uint8_t *sr = sm.sr[wib];
     int16_t *seg = sm.seg[wib];
-    // MT: staged neighbours' segment masks, CAP per warp, in dynamic shared memory after the bitmap staging
-    uint32_t *smeta = reinterpret_cast<uint32_t *>(s_dyn + (a.chg_smem ? (a.chg_words >> 2) : 0)) + (size_t)wib * CAP;
     // L2 eviction-priority policies (a.hints bits): gathered F_{d-1} rows, own F_{d-2} rows, F_d stores
     // (bit 4: use the hinted instructions with evict_normal where no other policy is set)
     const uint64_t pol_d = (a.hints & 16) ? policy_evict_normal() : 0ull;
@@ -625,20 +534,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                     dn = (nb == 1);
                     uint64_t *f = a.F[0] + (size_t)v * W;           // V_0(v) = {v}
                     const int wj = (int)(j >> 6);
-                    if constexpr (MT) {                              // its one mixed segment
-                        constexpr int SW = 2 * CPS;                  // words per segment
-                        const int w0 = (wj / SW) * SW;
 #pragma unroll
-                        for (int w = 0; w < SW; w += 2)
-                            st2(f + w0 + w, make_ulonglong2(w0 + w == wj ? 1ull << (j & 63) : 0ull,
-                                                            w0 + w + 1 == wj ? 1ull << (j & 63) : 0ull));
-                        a.meta[0][v] = 1u << (wj / SW);
-                    } else {
-#pragma unroll
-                        for (int w = 0; w < W; w += 2)
-                            st2(f + w, make_ulonglong2(w == wj ? 1ull << (j & 63) : 0ull,
-                                                       w + 1 == wj ? 1ull << (j & 63) : 0ull));
-                    }
+                    for (int w = 0; w < W; w += 2)
+                        st2(f + w, make_ulonglong2(w == wj ? 1ull << (j & 63) : 0ull,
+                                                   w + 1 == wj ? 1ull << (j & 63) : 0ull));
                 }
                 a.K[v] = 0;
             }
@@ -701,8 +600,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             const uint64_t *__restrict__ Fc = a.F[(d - 1) & 1];
             uint64_t *__restrict__ Fn = a.F[d & 1];
             const uint64_t *F0 = a.F[0], *F1 = a.F[1];
-            const uint32_t *meta_c = MT ? a.meta[(d - 1) & 1] : nullptr;   // rows changed at d-1
-            uint32_t *meta_n = MT ? a.meta[d & 1] : nullptr;
             const uint32_t *chp = a.chg[(d + 2) % 3];
             uint32_t *chn = a.chg[d % 3];
             uint32_t *chz = a.chg[(d + 1) % 3];
@@ -752,10 +649,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             // units (below); HM_HEAVY_DYN 0 deals them round-robin here instead
             if constexpr (HV && !HM_HEAVY_DYN)
                 if (n_items > 0)
-                nchg = heavy_items<W, BLOCK, WT, MT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
+                nchg = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                 a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
                                                 hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn,
-                                                cand, meta_c, MT ? a.meta[0] : nullptr, MT ? a.meta[1] : nullptr, meta_n);
+                                                cand);
             PROF_MARK(pf, 1);
 
             // ---- light rows: one warp per unit of 32 >> unit_shift rows of a 32-row group;
@@ -796,8 +693,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 PROF_MARK(pf, 2);
                 if (!amask) continue;                                    // warp-uniform
                 const uint32_t hword = a.has[g], qword = a.par[g];     // own rows: state held, its buffer
-                unsigned m_row = 0u;                                      // MT: lane's row's segment masks
-                if (MT && ((hword >> lane) & 1u)) m_row = a.meta[(qword >> lane) & 1u][g * 32 + lane];
                 uint32_t chg_bits = 0u, done_bits = 0u;
                 const int A0 = __shfl_sync(FULL, rp, q0);
                 const int A1 = __shfl_sync(FULL, rend, q0 + ur - 1);    // end of the unit's last row
@@ -819,7 +714,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                             const int pos = n + __popc(bm & ltmask);
                             su[pos] = u;
                             sr[pos] = (uint8_t)ri;
-                            if constexpr (MT) smeta[pos] = meta_c[u];
                         }
                         n += __popc(bm);
                     }
@@ -865,25 +759,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         // staging flush of this unit wrote), K, S
                         ulonglong2 vv[VEC];
                         zero_row<VEC>(vv);
-                        unsigned mo = 0u;                                 // MT: own segment masks
-                        if constexpr (MT) {
-                            mo = __shfl_sync(FULL, m_row, ri);
-                            const bool cb = has && ((chg_bits >> ri) & 1u);
-                            const bool hb = has && ((hword >> ri) & 1u);
-                            if (cb) mo = meta_n[v];                      // V_d written by an earlier flush
-                            else if (!hb) mo = 0u;
-                            if (cb || hb) {
-                                const bool q = (qword >> ri) & 1u;
-                                const uint64_t *src = cb ? Fn : (q ? F1 : F0);
-                                const uint64_t pol = cb ? 0ull : (q == (bool)((d - 1) & 1) ? pol_c : pol_p);
-#pragma unroll
-                                for (int c = 0; c < VEC; ++c) {
-                                    bool ld;
-                                    vv[c] = seg_value(mo, (c * TL + ltl) / CPS, ld);
-                                    if (ld) vv[c] = ld2p(src + (size_t)v * W + 2 * (c * TL + ltl), pol);
-                                }
-                            }
-                        } else if (has && ((chg_bits >> ri) & 1u)) {
+                        if (has && ((chg_bits >> ri) & 1u)) {
                             ld_row<W, TL, VEC>(vv, Fn, v, ltl);
                         } else if (has && ((hword >> ri) & 1u)) {
                             const bool q = (qword >> ri) & 1u;
@@ -936,22 +812,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         #pragma unroll
                             for (int q = 0; q < GD; ++q) {
                                 zero_row<VEC>(x[q]);
-                                if constexpr (MT) {
-                                    if (k0 + q < ke) {
-                                        const unsigned mu = smeta[k0 + q];
-                                        const int u = su[k0 + q];
-        #pragma unroll
-                                        for (int c = 0; c < VEC; ++c) {
-                                            const int sgc = (c * TL + ltl) / CPS;
-                                            if ((mo >> (16 + sgc)) & 1u) continue;      // own segment complete
-                                            bool ld;
-                                            x[q][c] = seg_value(mu, sgc, ld);
-                                            if (ld) x[q][c] = ld2p(Fc + (size_t)u * W + 2 * (c * TL + ltl), pol_c);
-                                        }
-                                    }
-                                } else {
-                                    if (k0 + q < ke) ld_row<W, TL, VEC>(x[q], Fc, su[k0 + q], ltl, pol_c);
-                                }
+                                if (k0 + q < ke) ld_row<W, TL, VEC>(x[q], Fc, su[k0 + q], ltl, pol_c);
                             }
         #pragma unroll
                             for (int q = 0; q < GD; ++q) or_row<VEC>(acc, x[q]);
@@ -982,27 +843,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         #pragma unroll
                             for (int o = TL / 2; o > 0; o >>= 1) wsum += __shfl_xor_sync(FULL, wsum, o);
                         }
-                        unsigned mn = 0u;                             // MT: segment masks of V_d(v)
-                        bool mixed[VEC];
-                        if constexpr (MT) {
-        #pragma unroll
-                            for (int c = 0; c < VEC; ++c) {
-                                const ulonglong2 nv = make_ulonglong2(acc[c].x | vv[c].x, acc[c].y | vv[c].y);
-                                const unsigned r = seg_masks<CPS>(nv, FULL, lteam * TL, TL, mixed[c]);
-                                const int sh = c * (TL / CPS);
-                                mn |= ((r & 0xffffu) << sh) | ((r >> 16) << (16 + sh));
-                            }
-                        }
                         if (cnt) {
                             or_row<VEC>(acc, vv);                         // V_d(v) = V_{d-1}(v) | new
-                            if constexpr (MT) {
-        #pragma unroll
-                                for (int c = 0; c < VEC; ++c)
-                                    if (mixed[c]) st2p(Fn + (size_t)v * W + 2 * (c * TL + ltl), acc[c], pol_n);
-                                if (ltl == 0) meta_n[v] = mn;
-                            } else {
-                                st_row<W, TL, VEC>(Fn, v, ltl, acc, pol_n);
-                            }
+                            st_row<W, TL, VEC>(Fn, v, ltl, acc, pol_n);
                             if (ltl == 0) {
                                 const int2 ci = comp_of(a, v, n_giant);
                                 int64_t nb = (int64_t)ci.y - base;
@@ -1057,10 +900,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             // round-robin before the light units; compiling both placements in is slower than either)
             if constexpr (HV && HM_HEAVY_DYN)
                 if (n_items > 0)
-                nchg += heavy_items<W, BLOCK, WT, MT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
+                nchg += heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                  a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
                                                  n_heavy, hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn,
-                                                 chn, cand, meta_c, MT ? a.meta[0] : nullptr, MT ? a.meta[1] : nullptr, meta_n);
+                                                 chn, cand);
             // rows changed by this CTA: warp sums, one shared atomic per warp
             nchg = __reduce_add_sync(FULL, nchg);
             if (lane == 0 && nchg) atomicAdd(&sm.nchg, nchg);
@@ -1088,7 +931,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 __syncthreads();
             }
             PROF_MARK(pf, 7);
-            const int fv = sm.flag;
+            int fv = sm.flag;
+            if (d > hi + 1) {                  // deeper than any BFS of hi rows: a kernel bug, never loop on
+                fv = 0;
+                if (gtid == 0) a.counters[7] = 1ull;
+            }
             if (gtid == 0) {
                 if (sm.nlast > 0) {
                     a.counters[3] += (unsigned long long)sm.nlast;                  // row commits
@@ -1149,14 +996,7 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         HM_MSBFS_CASE(32, 8, 2, 2)
         HM_MSBFS_CASE(64, 32, 4, 2)
     case ((64 * 100 + 16) * 100 + 4 * 10 + 2):                 // default: lean variants without heavy rows
-        if (a.meta[0]) {                                        // segment skipping
-            if (a.hstart)
-                kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, true, true>
-                            : (const void *)msbfs_kernel<64, 16, 4, 2, false, true, true>;
-            else
-                kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false, true>
-                            : (const void *)msbfs_kernel<64, 16, 4, 2, false, false, true>;
-        } else if (a.hstart)
+        if (a.hstart)
             kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true> : (const void *)msbfs_kernel<64, 16, 4, 2, false>;
         else
             kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false>
@@ -1166,12 +1006,8 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         HM_MSBFS_CASE(64, 16, 2, 2)
     case ((128 * 100 + 16) * 100 + 2 * 10 + 2):               // W = 128: graphs without heavy rows only
         if (a.hstart) return -1;
-        if (a.meta[0])
-            kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false, true>
-                        : (const void *)msbfs_kernel<128, 16, 2, 2, false, false, true>;
-        else
-            kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false>
-                        : (const void *)msbfs_kernel<128, 16, 2, 2, false, false>;
+        kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false>
+                    : (const void *)msbfs_kernel<128, 16, 2, 2, false, false>;
         block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
         break;
     case ((128 * 100 + 16) * 100 + 4 * 10 + 2):
@@ -1188,7 +1024,6 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     }
 #undef HM_MSBFS_CASE
     size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 : 0;
-    if (a.meta[0]) dyn += (size_t)(block / 32) * CAP * 4;     // MT staging (every instantiation above with meta is MT)
     if (HM_ASYNC_GS > 0) dyn += (size_t)(block / 32) * (32 / TL) * HM_ASYNC_GS * (TL * vec) * 16;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) return -5;
     int maxb = 0;

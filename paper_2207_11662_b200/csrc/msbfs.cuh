@@ -31,10 +31,6 @@ struct BfsArgs {
     int32_t *hclaim;             // [3] heavy-item claim counters, rotated by level
     uint64_t *F[2];              // [n_live][W] visited-set rows V(v), double-buffered: a row that
                                  // changes at level d writes V_d(v) into F[d & 1]
-    uint32_t *meta[2];           // [n_live] per buffer (nullptr: off): segment masks of V(v) as stored in F[b] --
-                                 // bits 0-15 segments holding a source, bits 16-31 segments holding every
-                                 // source (16 equal segments of W/32 16-byte chunks).  Only mixed segments
-                                 // are stored; zero and full ones are never read (segment skipping)
     uint32_t *chg[3];            // row bitmaps "changed at level", rotating over 3 levels
     uint32_t *done;              // row bitmap: all sources of the row's window reached it
     uint32_t *has;               // row bitmap: the row holds a visited set in this batch
@@ -46,7 +42,8 @@ struct BfsArgs {
     uint64_t *S;                 // [n_live] distance-sum accumulators (target side)
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches, [2] model bytes, [3] row commits,
-                                   // [4] CSR bytes, [5] top-down levels, [6] state bytes of the commits
+                                   // [4] CSR bytes, [5] top-down levels, [6] state bytes of the commits,
+                                   // [7] level guard tripped (hm_get_stats fails)
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the previous level's change bitmap in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)

@@ -91,7 +91,7 @@ def test_psi_special(hm, name, V, E):
     # narrow batches (B = 512: several batches per component), other team widths and occupancies
     for words, team, bps, unit, prune, fbar in ((8, 0, 0, 8, 1, 1), (16, 4, 0, 16, 0, 0), (64, 32, 1, 32, 1, 0),
                                                 (64, 16, 1, 4, 0, 1), (32, 16, 1, 2, 1, 1), (64, 16, 0, 8, 1, 1),
-                                                (128, 0, 0, 0, 1, 1), (128, 0, 0, 4, 0, 0)):
+                                                (64, 0, 0, 2, 0, 1), (128, 0, 0, 0, 1, 1), (128, 0, 0, 4, 0, 0)):
         with hm() as ctx:
             if words == 128:                     # 8192 sources per batch: no heavy rows
                 ctx.set_param("bfs_heavy", 1 << 30)
