@@ -89,6 +89,8 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   bottom-up over every row not yet complete; 0 = always bottom-up
  *   "bfs_fuse"    : hm_closeness_multi: 0 one pass per graph, 1 one fused pass over the disjoint union,
  *                   2 (default) fused when sum of V <= 2^17 (graphs too small to fill the GPU alone)
+ *   "bfs_count_rows": 1 runs the default MS-BFS kernels in a counting instantiation that fills hm_stats
+ *                   bfs_gathers / bfs_own_reads (the row traffic; ~3 % slower), 0 (default) the timed ones
  *   "topk_tiles"  : top-K lists (K <= 4096, n > 4096): 1 (default) one launch -- per-tile block-local radix
  *                   selects, then the last tile merges and sorts -- where the G = ceil(n / 8192) tiles' K
  *                   candidates fit one block (G * K <= 16384), 0 the cooperative 12-pass radix select
@@ -289,6 +291,11 @@ typedef struct {
     double phase_ms[10];      /* with timing = 2: CUDA-event time per phase -- [0] components, [1] pruning
                                  decision, [2] relabel, [3] MS-BFS setup, [4] MS-BFS, [5] finalize + mean +
                                  CC nodes, [6] compose, [7] top-K, [8] aggregation, [9] other */
+    int64_t bfs_gathers;      /* neighbour rows gathered (one 8 W-byte row read each), summed over levels and
+                                 batches: with bfs_own_reads and bfs_row_commits the MS-BFS's row traffic
+                                 through L2, 8 W (gathers + own reads + commits) bytes; counted only with
+                                 "bfs_count_rows" 1 (default kernels), else 0 */
+    int64_t bfs_own_reads;    /* own visited-set rows read (rows with a state and a changed neighbour) */
 } hm_stats;
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset);
 

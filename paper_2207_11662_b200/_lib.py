@@ -25,7 +25,8 @@ class HmStats(ctypes.Structure):
                 ("bfs_model_bytes", ctypes.c_double), ("bfs_row_commits", ctypes.c_int64),
                 ("bfs_csr_bytes", ctypes.c_double), ("bfs_td_levels", ctypes.c_int64),
                 ("bfs_state_bytes", ctypes.c_double), ("host_syncs", ctypes.c_int64),
-                ("phase_ms", ctypes.c_double * 10)]
+                ("phase_ms", ctypes.c_double * 10), ("bfs_gathers", ctypes.c_int64),
+                ("bfs_own_reads", ctypes.c_int64)]
 
 
 # name -> (restype, argtypes); must match include/hm.h (tests/test_abi.py checks the names)

@@ -1217,6 +1217,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.nshards = nshards;
     a.interleave = ctx->params.bfs_interleave;
     a.dbg_level = ctx->params.bfs_dbg >> 8;                   // bfs_dbg bits 8.. (profiling builds)
+    a.count_rows = ctx->params.bfs_count_rows;
     {
         // rows per work unit: bfs_unit, or (0, auto) about a quarter of the live rows per warp of
         // a full grid (2 CTAs x 14 warps per SM), as a power of two in [2, 32], 16 taken as 32.

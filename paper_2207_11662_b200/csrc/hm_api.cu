@@ -85,8 +85,8 @@ hm_status hm_create(hm_ctx **out, int device, void *cuda_stream) {
         HM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         HM_CUDA(cudaEventCreate(&ctx->ev0));
         HM_CUDA(cudaEventCreate(&ctx->ev1));
-        ctx->dstats.alloc(64, ctx->stream);
-        HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));
+        ctx->dstats.alloc(128, ctx->stream);
+        HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 128, ctx->stream));
         HM_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (const hm::Error &) {
         hm_destroy(ctx);
@@ -137,6 +137,8 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
     } else if (n == "bfs_prune") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_prune must be 0, 1 or 2 (auto)");
         ctx->params.bfs_prune = (int)value;
+    } else if (n == "bfs_count_rows") {
+        ctx->params.bfs_count_rows = value ? 1 : 0;
     } else if (n == "topk_tiles") {
         ctx->params.topk_tiles = value ? 1 : 0;
     } else if (n == "bfs_fuse") {
@@ -478,8 +480,8 @@ hm_status hm_sync(hm_ctx *ctx) {
 hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     HM_API_BEGIN(ctx)
     HM_REQUIRE(out, HM_EINVAL, "null out");
-    unsigned long long dv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long dv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    HM_CUDA(cudaMemcpyAsync(dv, ctx->dstats.p, 80, cudaMemcpyDeviceToHost, ctx->stream));
     HM_CUDA(cudaStreamSynchronize(ctx->stream));
     // the MS-BFS level guard (a level deeper than the batch's rows): results since the last reset are wrong
     HM_REQUIRE(dv[7] == 0, HM_ECUDA, "MS-BFS level guard tripped: a BFS ran deeper than its rows (kernel bug)");
@@ -511,10 +513,12 @@ hm_status hm_get_stats(hm_ctx *ctx, hm_stats *out, int reset) {
     out->bfs_csr_bytes = (double)dv[4];
     out->bfs_td_levels = (int64_t)dv[5];
     out->bfs_state_bytes = (double)dv[6];
+    out->bfs_gathers = (int64_t)dv[8];
+    out->bfs_own_reads = (int64_t)dv[9];
     if (reset) {
         ctx->stats = Stats();
         for (int i = 0; i < 10; ++i) ctx->phase_ms[i] = 0.0;
-        HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 64, ctx->stream));
+        HM_CUDA(cudaMemsetAsync(ctx->dstats.p, 0, 128, ctx->stream));
         HM_CUDA(cudaStreamSynchronize(ctx->stream));
     }
     HM_API_END(ctx)

@@ -162,6 +162,7 @@ struct Smem {
     unsigned long long lb[4];    // counting barrier (thread 0): expected arrivals [p], changed rows seen [2 + p]
     unsigned long long epoch;    // counting barriers passed (thread 0); parity p = epoch & 1
     int nchg;                    // rows this CTA changed in the current level
+    unsigned ngat, nown;         // rows this CTA gathered / own rows it read in the current level
     long long nlast;             // rows the whole grid changed before the last counting barrier
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
@@ -269,6 +270,16 @@ __device__ __forceinline__ void count_barrier(unsigned long long *lbar, SM &sm, 
     __threadfence();
 }
 
+// Level guard (thread 0, after the level barrier): no BFS over hi rows runs deeper than hi levels, so
+// a deeper level is a kernel bug -- stop the batch rather than loop on, and flag it (hm_get_stats fails)
+template <class SM>
+__device__ __forceinline__ void level_guard(SM &sm, int d, unsigned long long *counters) {
+    if (d > sm.hi + 1) {
+        sm.flag = 0;
+        counters[7] = 1ull;
+    }
+}
+
 // Top-down discovery for a sparse level (direction optimisation): every row that changed at
 // d-1 (the frontier, bitmap chp) marks its neighbours that are not done as candidates; the
 // level's pull step then visits candidate rows only.  Warp per 32-row frontier group, striding
@@ -311,7 +322,8 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
                                  int hi, int n_giant, int64_t base, int d, const uint32_t *chp_s,
                                  uint32_t *has, uint32_t *par, const uint64_t *__restrict__ Fc,
                                  const uint64_t *F0, const uint64_t *F1, uint64_t *__restrict__ Fn,
-                                 uint32_t *chn, const uint32_t *cand) {
+                                 uint32_t *chn, const uint32_t *cand, unsigned *s_ngat) {
+    // s_ngat: the CTA's gather and own-read counters (Smem ngat, nown)
     constexpr int T = W / 2;
     constexpr int TPB = BLOCK / T;
     constexpr int64_t B = 64 * W;
@@ -357,6 +369,7 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
                 c = bit_of(chp_s, u);
             }
             unsigned m = __ballot_sync(tmask, c) >> tbase;
+            if (s_ngat && tl == 0 && m) atomicAdd(s_ngat, (unsigned)__popc(m));
             while (m) {                                          // HGD neighbour rows in flight
                 int uq[HGD];
         #pragma unroll
@@ -411,7 +424,10 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
         if (tib == 0) {
             // own visited set V_{d-1}(v): in the buffer of the level that last wrote it
             ulonglong2 vv = make_ulonglong2(0ull, 0ull);
-            if (bit_of(has, v)) vv = ld2((bit_of(par, v) ? F1 : F0) + (size_t)v * W + 2 * tl);
+            if (bit_of(has, v)) {
+                vv = ld2((bit_of(par, v) ? F1 : F0) + (size_t)v * W + 2 * tl);
+                if (s_ngat && tl == 0) atomicAdd(s_ngat + 1, 1u);
+            }
             const ulonglong2 nw = make_ulonglong2(acc.x & ~vv.x, acc.y & ~vv.y);
             int cnt = __popcll(nw.x) + __popcll(nw.y);
 #pragma unroll
@@ -457,7 +473,10 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
 // WT: weighted sums for the pruned component (prune.cu): S(v) += d * sum over the new
 // sources s of (1 + T(s)), the T sum taken from per-batch bit planes of T in shared memory
 // HV: heavy-row path compiled in (false only for graphs without heavy rows: a leaner kernel)
-template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
+// CNT: count the row traffic (gathered rows, own rows read) into counters[8..9] -- a separate
+// instantiation, so the timed kernels carry none of it (it costs them ~3 %)
+template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, bool CNT = false,
+          int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2 < 32 ? W / 2 : 32;   // lanes per row in the heavy path (W <= 64 with heavy rows)
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
@@ -615,6 +634,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             if (threadIdx.x == 0) {
                 sm.next = a.interleave ? 0 : (int)(((int64_t)blockIdx.x * (ngroups << a.unit_shift)) / gridDim.x);
                 sm.nchg = 0;
+                sm.ngat = 0u;
+                sm.nown = 0u;
             }
             if (a.chg_smem) {
                 const int nw4 = (int)((ngroups + 3) >> 2);
@@ -652,7 +673,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 nchg = heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                 a.K, a.S, nullptr, &s_red[0][0], &s_pl[0][0], s_nb, n_items, n_heavy,
                                                 hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn, chn,
-                                                cand);
+                                                cand, CNT ? &sm.ngat : nullptr);
             PROF_MARK(pf, 1);
 
             // ---- light rows: one warp per unit of 32 >> unit_shift rows of a 32-row group;
@@ -720,6 +741,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                     const bool flush = (n > CAP - 32 * SCAN_U) || (a0 + 32 * SCAN_U >= A1);
                     PROF_MARK(pf, 3);
                     if (!flush || n == 0) continue;
+                    if (CNT && lane == 0) atomicAdd(&sm.ngat, (unsigned)n);  // this flush's gathers
                     __syncwarp();
                     // segments: runs of equal row index (at most 32)
                     int nseg = 0;
@@ -732,6 +754,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                     }
                     if (lane == 0) seg[nseg] = (int16_t)n;
                     __syncwarp();
+                    if constexpr (CNT) {                                       // own rows read this flush
+                        const bool own = lane < nseg && (((hword | chg_bits) >> sr[seg[lane]]) & 1u);
+                        const unsigned ob = __ballot_sync(FULL, own);
+                        if (lane == 0 && ob) atomicAdd(&sm.nown, (unsigned)__popc(ob));
+                    }
                     // sort the segments by length (descending) so the TPW rows of a
                     // lock-step round have similar neighbour counts
                     int key = lane < nseg ? (((seg[lane + 1] - seg[lane]) << 5) | lane) : -1;
@@ -903,12 +930,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 nchg += heavy_items<W, BLOCK, WT>(a.row_ptr, a.col, a.cinfo, a.heavy, a.hstart, a.hacc, a.hcnt, a.done,
                                                  a.K, a.S, a.hclaim + (d % 3), &s_red[0][0], &s_pl[0][0], s_nb, n_items,
                                                  n_heavy, hi, n_giant, base, d, chp_s, a.has, a.par, Fc, F0, F1, Fn,
-                                                 chn, cand);
+                                                 chn, cand, CNT ? &sm.ngat : nullptr);
             // rows changed by this CTA: warp sums, one shared atomic per warp
             nchg = __reduce_add_sync(FULL, nchg);
             if (lane == 0 && nchg) atomicAdd(&sm.nchg, nchg);
             __syncthreads();
             const int nchg_cta = sm.nchg;
+            if (CNT && threadIdx.x == 0) {                               // row traffic of this CTA's level
+                if (sm.ngat) atomicAdd(a.counters + 8, (unsigned long long)sm.ngat);
+                if (sm.nown) atomicAdd(a.counters + 9, (unsigned long long)sm.nown);
+            }
             // one flag write per CTA (same-address stores from every group serialise in L2)
             if (nchg_cta && threadIdx.x == 0 && !a.lbar) a.flags[d % 3] = 1;
 #ifdef HM_MSBFS_PROF
@@ -920,22 +951,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
 #endif
             PROF_MARK(pf, 6);
             if (a.lbar) {
-                if (threadIdx.x == 0) count_barrier(a.lbar, sm, nchg_cta);   // sm.nlast = rows changed at d
+                if (threadIdx.x == 0) {
+                    count_barrier(a.lbar, sm, nchg_cta);                      // sm.nlast = rows changed at d
+                    level_guard(sm, d, a.counters);
+                }
                 __syncthreads();
             } else {
                 grid.sync();
                 if (threadIdx.x == 0) {
                     sm.flag = *((volatile int32_t *)(a.flags + (d % 3)));
                     sm.nlast = -1;                                   // unknown without the counting barrier
+                    level_guard(sm, d, a.counters);
                 }
                 __syncthreads();
             }
             PROF_MARK(pf, 7);
-            int fv = sm.flag;
-            if (d > hi + 1) {                  // deeper than any BFS of hi rows: a kernel bug, never loop on
-                fv = 0;
-                if (gtid == 0) a.counters[7] = 1ull;
-            }
+            const int fv = sm.flag;
             if (gtid == 0) {
                 if (sm.nlast > 0) {
                     a.counters[3] += (unsigned long long)sm.nlast;                  // row commits
@@ -996,7 +1027,14 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         HM_MSBFS_CASE(32, 8, 2, 2)
         HM_MSBFS_CASE(64, 32, 4, 2)
     case ((64 * 100 + 16) * 100 + 4 * 10 + 2):                 // default: lean variants without heavy rows
-        if (a.hstart)
+        if (a.count_rows) {                                     // row-traffic counting instantiations
+            if (a.hstart)
+                kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, true, true>
+                            : (const void *)msbfs_kernel<64, 16, 4, 2, false, true, true>;
+            else
+                kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false, true>
+                            : (const void *)msbfs_kernel<64, 16, 4, 2, false, false, true>;
+        } else if (a.hstart)
             kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true> : (const void *)msbfs_kernel<64, 16, 4, 2, false>;
         else
             kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false>
@@ -1006,8 +1044,12 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         HM_MSBFS_CASE(64, 16, 2, 2)
     case ((128 * 100 + 16) * 100 + 2 * 10 + 2):               // W = 128: graphs without heavy rows only
         if (a.hstart) return -1;
-        kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false>
-                    : (const void *)msbfs_kernel<128, 16, 2, 2, false, false>;
+        if (a.count_rows)
+            kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false, true>
+                        : (const void *)msbfs_kernel<128, 16, 2, 2, false, false, true>;
+        else
+            kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false>
+                        : (const void *)msbfs_kernel<128, 16, 2, 2, false, false>;
         block = a.tw ? BLOCK_WEIGHTED : BLOCK_PLAIN;
         break;
     case ((128 * 100 + 16) * 100 + 4 * 10 + 2):

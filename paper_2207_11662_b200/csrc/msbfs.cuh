@@ -43,7 +43,8 @@ struct BfsArgs {
     int32_t *flags;              // [3] any-change flags, rotated by level
     unsigned long long *counters;  // [0] levels, [1] batches, [2] model bytes, [3] row commits,
                                    // [4] CSR bytes, [5] top-down levels, [6] state bytes of the commits,
-                                   // [7] level guard tripped (hm_get_stats fails)
+                                   // [7] level guard tripped (hm_get_stats fails), [8] rows gathered,
+                                   // [9] own rows read
     unsigned long long *dbgc;    // debug (bfs_dbg & 2): per-level counts and times (+ phase cycles)
     int chg_smem;                // 1: stage the previous level's change bitmap in dynamic shared memory
     int chg_words;               // bitmap words (multiple of 4)
@@ -57,6 +58,7 @@ struct BfsArgs {
     unsigned long long *lbar;    // [4] counting grid-barrier counters (zeroed): arrivals [p] and changed rows
                                  // [2 + p] by barrier-epoch parity p; nullptr: grid.sync + flag (no top-down)
     int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)
+    int count_rows;              // 1: run the row-traffic counting instantiation (default kernels; counters[8..9])
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per
