@@ -856,7 +856,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         for (int o = TL / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
                         unsigned long long wsum = 0ull;   // sum of T over the new sources (pruned component)
                         if constexpr (WT) {
-                            const int nbp = (has && v < n_giant) ? s_nb : 0;
+                            // (rows without new sources skip the planes: cnt is team-uniform here)
+                            const int nbp = (has && cnt && v < n_giant) ? s_nb : 0;
                             const int nbw = __reduce_max_sync(FULL, (unsigned)nbp);   // warp-uniform trip count
                             for (int b = 0; b < nbw; ++b) {
                                 unsigned c2 = 0;

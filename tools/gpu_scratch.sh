@@ -1,7 +1,17 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/gputests.log
-for c in C1 C2 C3; do
-  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b_$c.log 2>&1
-  echo "$c rc=$?"; tail -1 gpurun_out/b_$c.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d.get('cuda_graph'), d['roofline']['frac'], d['roofline'].get('fused_graphs'))"
+for cap in 0 4 100; do
+HM_DEFINES="HM_PLANE_CAP=$cap" python -m paper_2207_11662_b200.build --force > gpurun_out/build.log 2>&1 || exit 1
+python - <<'PY'
+import sys; sys.path.insert(0, '.')
+from paper_2207_11662_b200 import Context
+from synth import build_config
+h = build_config("C5")
+with Context(0) as ctx:
+    ctx.set_param("timing", 1)
+    ctx.load_layers(h.V, h.layers)
+    g = ctx.and_aggregate([0, 1, 2])
+    ctx.closeness(g); ctx.sync(); ctx.stats(reset=True)
+    ctx.closeness(g); ctx.sync(); st = ctx.stats(reset=True)
+    print("AND", {k: st[k] for k in ("bfs_ms", "bfs_levels")})
+PY
 done
-python -c "import __graft_entry__ as g; g.smoke()"
+python -m paper_2207_11662_b200.build --force > /dev/null 2>&1
