@@ -264,20 +264,34 @@ __global__ void k_nlive(const int32_t *size_s, const int32_t *cstart, int32_t *s
 
 // vertex keys: component rank (value: the vertex; the stable sort keeps ids ascending inside a
 // component); peeled vertices (rem[v] > 0) key V, after every component: no BFS row
-__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, const int32_t *rem, uint32_t *key,
-                            uint32_t *val, int V) {
+// vertex keys: component rank (stable: vertex id within a component).  With tsz (pruned graphs) the key
+// is rank << 8 | (255 - min(T, 255)) in the pruned (rank-0) component: its core rows sorted by hanging-tree
+// size T descending, so a batch window's T is constant over long runs of sources (the MS-BFS then weighs
+// a 128-source chunk by T x popc instead of T's bit planes)
+__global__ void k_vert_keys(const int32_t *label, const int32_t *rank_of_root, const int32_t *rem,
+                            const uint32_t *tsz, uint32_t *key, uint32_t *val, int V) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
-        key[v] = (rem && rem[v]) ? (uint32_t)V : (uint32_t)rank_of_root[label[v]];
+        if (tsz) {
+            if (rem[v]) {
+                key[v] = (uint32_t)V << 8;
+            } else {
+                const uint32_t r = (uint32_t)rank_of_root[label[v]];
+                const uint32_t t = tsz[v] - 1u;
+                key[v] = (r << 8) | (r == 0 ? 255u - (t < 255u ? t : 255u) : 0u);
+            }
+        } else {
+            key[v] = (rem && rem[v]) ? (uint32_t)V : (uint32_t)rank_of_root[label[v]];
+        }
         val[v] = (uint32_t)v;
     }
 }
 
 __global__ void k_perm(const uint32_t *rk, const uint32_t *olds, const int32_t *row_ptr, const int32_t *degl,
                        const int32_t *size_s, const int32_t *cstart, int32_t *new_to_old, int32_t *old_to_new,
-                       int32_t *new_deg, int2 *cinfo, int V) {
+                       int32_t *new_deg, int2 *cinfo, int V, int kshift) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
         const int old = (int)olds[i];
-        const int r = (int)rk[i];
+        const int r = (int)(rk[i] >> kshift);              // component rank (k_vert_keys)
         new_to_old[i] = old;
         old_to_new[old] = i;
         if (r >= V) {                       // peeled vertex: no row
@@ -1033,8 +1047,10 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     count_launch(ctx);
     {
         const int kbits = sh;                                      // keys <= V
+        // pruned graphs: vertex keys carry the core's T order in 8 more bits (k_vert_keys)
+        const int kshift = (pr.active && sh + 8 <= 32) ? 8 : 0;
         size_t tb = 0;
-        HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, V, 0, kbits, s));
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, V, 0, kbits + kshift, s));
         size_t tb2 = 0;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, size_s.as<int32_t>(), cstart.as<int32_t>(), V + 1, s));
         if (tb2 > tb) tb = tb2;
@@ -1045,12 +1061,13 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, size_s.as<int32_t>(), cstart.as<int32_t>(), V, s));
         k_nlive<<<gb, TB, 0, s>>>(size_s.as<int32_t>(), cstart.as<int32_t>(), scalars, V);
-        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem, kin, vin, V);
+        k_vert_keys<<<gb, TB, 0, s>>>(label.as<int32_t>(), rank.as<int32_t>(), rem,
+                                      kshift ? pr.tsz.as<uint32_t>() : nullptr, kin, vin, V);
         tbs = tb;
-        HM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tbs, kin, kout, vin, vout, V, 0, kbits, s));
+        HM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tbs, kin, kout, vin, vout, V, 0, kbits + kshift, s));
         k_perm<<<gb, TB, 0, s>>>(kout, vout, U.rp, pr.active ? pr.degl.as<int32_t>() : nullptr,
                                 size_s.as<int32_t>(), cstart.as<int32_t>(), n2o.as<int32_t>(), o2n.as<int32_t>(),
-                                ndeg.as<int32_t>(), cinfo.as<int2>(), V);
+                                ndeg.as<int32_t>(), cinfo.as<int2>(), V, kshift);
         tbs = tb;
         HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbs, ndeg.as<int32_t>(), nrp.as<int32_t>(), V + 1, s));
         check_launch("relabel");
@@ -1201,17 +1218,20 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.K = Kb.as<uint16_t>();
     a.chg_words = (int)bmw;
     a.hints = ctx->params.bfs_hints;
-    Buf Trow, planes;
+    Buf Trow, planes, tconst;
     a.tw = nullptr;
     a.planes = nullptr;
+    a.tconst = nullptr;
     if (pr.active) {                    // weights 1 + T(s) of the pruned MS-BFS (prune.cu (1))
         Trow.alloc((size_t)V * 4, s);
         planes.alloc((size_t)BFS_T_BITS * W * 8, s);
+        tconst.alloc((size_t)(W / 2) * 4 + 16, s);
         k_row_T<<<gb, TB, 0, s>>>(n2o.as<int32_t>(), pr.tsz.as<uint32_t>(), scalars, Trow.as<uint32_t>());
         check_launch("k_row_T");
         count_launch(ctx);
         a.tw = Trow.as<uint32_t>();
         a.planes = planes.as<unsigned long long>();
+        a.tconst = tconst.as<int32_t>();
     }
     a.shard = shard;
     a.nshards = nshards;

@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     __shared__ Smem<BLOCK / 32> sm;
     __shared__ unsigned long long s_pl[WT ? BFS_T_BITS : 1][WT ? W : 1];   // T bit planes of the batch window
     __shared__ int s_nb;
+    __shared__ int s_tc[WT ? W / 2 : 1];   // T of each 128-source chunk of the window when constant, else -1
 #ifdef HM_MSBFS_PROF
     __shared__ int s_tmin, s_tmax;
 #endif
@@ -585,6 +586,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                     if (lane == 0) a.planes[(size_t)b * W + w] = (unsigned long long)lo | ((unsigned long long)hi1 << 32);
                 }
             }
+            // chunks of 128 sources (words 2c, 2c+1) with one T: the core rows are sorted by T (k_vert_keys),
+            // so nearly all are, and a commit weighs them by T x popc instead of the planes
+            for (int64_t c = gwarp; c < W / 2; c += nwarps) {
+                unsigned tmin = 0xffffffffu, tmax = 0u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t r = base + 128 * c + 32 * k + lane;
+                    if (r < n_giant) {
+                        const uint32_t t = a.tw[r];
+                        tmin = min(tmin, t);
+                        tmax = max(tmax, t);
+                    }
+                }
+                tmin = __reduce_min_sync(FULL, tmin);
+                tmax = __reduce_max_sync(FULL, tmax);
+                if (lane == 0) a.tconst[c] = tmin == 0xffffffffu ? 0 : (tmin == tmax ? (int)tmin : -1);
+            }
         }
         if (a.lbar) {                                                // the level-0 frontier: the sources
             if (threadIdx.x == 0) sm.nchg = 0;
@@ -606,6 +624,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 s_pl[i / W][i % W] = x;
                 if (x) atomicMax(&s_nb, i / W + 1);
             }
+            for (int i = threadIdx.x; i < W / 2; i += BLOCK) s_tc[i] = a.tconst[i];
             __syncthreads();
         }
 
@@ -856,15 +875,26 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         for (int o = TL / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
                         unsigned long long wsum = 0ull;   // sum of T over the new sources (pruned component)
                         if constexpr (WT) {
-                            // (rows without new sources skip the planes: cnt is team-uniform here)
-                            const int nbp = (has && cnt && v < n_giant) ? s_nb : 0;
+                            // chunks of one T: T x popc; the others by T's bit planes (rows without new
+                            // sources skip both: cnt is team-uniform here)
+                            int needp = 0;
+                            if (has && cnt && v < n_giant) {
+        #pragma unroll
+                                for (int q = 0; q < VEC; ++q) {
+                                    const int t = s_tc[q * TL + ltl];
+                                    if (t >= 0) wsum += (unsigned long long)t * (unsigned)(__popcll(acc[q].x) + __popcll(acc[q].y));
+                                    else needp = 1;
+                                }
+                            }
+                            const int nbp = needp ? s_nb : 0;
                             const int nbw = __reduce_max_sync(FULL, (unsigned)nbp);   // warp-uniform trip count
                             for (int b = 0; b < nbw; ++b) {
                                 unsigned c2 = 0;
         #pragma unroll
                                 for (int q = 0; q < VEC; ++q) {
                                     const int wi = 2 * (q * TL + ltl);
-                                    c2 += __popcll(acc[q].x & s_pl[b][wi]) + __popcll(acc[q].y & s_pl[b][wi + 1]);
+                                    if (s_tc[q * TL + ltl] < 0)
+                                        c2 += __popcll(acc[q].x & s_pl[b][wi]) + __popcll(acc[q].y & s_pl[b][wi + 1]);
                                 }
                                 if (b < nbp) wsum += (unsigned long long)c2 << b;
                             }

@@ -53,6 +53,7 @@ struct BfsArgs {
     int interleave;              // 1: CTA b owns units b, b + grid, ...; 0: a contiguous range
     const uint32_t *tw;          // pruned MS-BFS: hanging-tree size T per row (nullptr: unweighted)
     unsigned long long *planes;  // [BFS_T_BITS][W] scratch: T bit planes of the batch window
+    int32_t *tconst;             // [W/2] scratch: per 128-source chunk of the window, its T if constant, else -1
     int hints;                   // L2 policy bits: 1 gathers evict_last, 2 own F_{d-2} evict_first,
                                  // 4 F_d stores evict_last, 8 F_d stores evict_first, 16 evict_normal
     unsigned long long *lbar;    // [4] counting grid-barrier counters (zeroed): arrivals [p] and changed rows
