@@ -88,9 +88,13 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   then only candidate rows pull -- when frontier rows * bfs_td <= the batch's rows, else
  *                   bottom-up over every row not yet complete; 0 = always bottom-up
  *   "bfs_fuse"    : hm_closeness_multi: 0 one pass per graph, 1 one fused pass over the disjoint union,
- *                   2 (default) fused when sum of V <= 2^17 (graphs too small to fill the GPU alone)
+ *                   2 (default) fused when sum of V <= 2^17 (graphs too small to fill the GPU alone), else
+ *                   graphs known to run unpruned fused in groups of <= 2^17 vertices, the rest one pass each
  *   "bfs_count_rows": 1 runs the default MS-BFS kernels in a counting instantiation that fills hm_stats
  *                   bfs_gathers / bfs_own_reads (the row traffic; ~3 % slower), 0 (default) the timed ones
+ *   "bfs_torder"  : pruned graphs: relabel the pruned core in order of hanging-tree size T so the MS-BFS weighs
+ *                   128-source chunks by T x popc (0 never, 1 (default) graphs without rows above degree 256,
+ *                   2 always)
  *   "topk_tiles"  : top-K lists (K <= 4096, n > 4096): 1 (default) one launch -- per-tile block-local radix
  *                   selects, then the last tile merges and sorts -- where the G = ceil(n / 8192) tiles' K
  *                   candidates fit one block (G * K <= 16384), 0 the cooperative 12-pass radix select
@@ -160,8 +164,10 @@ hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reac
  * (the layers of a HoMLN, analysed "in parallel", plus any
  * aggregate).  Fused ("bfs_fuse" 1, or 2 = default when sum of V <= 2^17):
  * their all-sources BFS runs over the disjoint union in ONE pass and shares
- * every level step (no pruning, no host round trip); otherwise one hm_closeness
- * pass per graph.  Results are per graph, identical to n separate hm_closeness
+ * every level step (no pruning, no host round trip); otherwise (default) the
+ * graphs known not to be pruned (an earlier call's cached decision) are fused
+ * in groups of <= 2^17 vertices and every other graph gets its own
+ * hm_closeness pass.  Results are per graph, identical to n separate hm_closeness
  * calls either way, cached for hm_compose / hm_topk_closeness / hm_cc_nodes and
  * readable with hm_closeness_results.  graph_ids: host array.  Errors: n < 1 or
  * repeated id -> EINVAL; unknown id -> ESTATE; fused with n > 64 -> EINVAL;

@@ -821,20 +821,45 @@ void closeness(hm_ctx *ctx, Graph &G) { closeness_multi(ctx, std::vector<Graph *
 
 // Fusing pays while the graphs are too small to fill the GPU one at a time (C2, 4 graphs of 16 K
 // vertices: 3.24 -> 1.77 ms per step; C1, 3 graphs of 1000 vertices: 0.55 ms with three one-CTA
-// small-path passes, 0.42 ms fused); larger graphs each fill the grid, keep their own pruning (the
-// fused pass does not prune) and their state rows stay L2-resident (C3, 14 graphs of 64 K vertices:
-// 41.1 ms separately, 57.8 ms fused).
+// small-path passes, 0.42 ms fused).  Larger graphs fill the grid on their own and keep their own
+// pruning (the fused pass does not prune): C3's 14 graphs fused take 57.8 ms, separately 39.9.  Among
+// them, graphs whose (cached) pruning decision is "no pruning" still gain from sharing level steps in
+// groups of <= 2^17 vertices (C3's two ER layers: 17.4 -> 13.6 ms fused), while pruned ones lose
+// (C3's R-MAT layers 6.8 -> 8.8, C4's layers 48.7 -> 65.0) and run one pass each.
 constexpr int64_t FUSE_AUTO_MAX_V = (int64_t)1 << 17;
+static bool known_unpruned(hm_ctx *ctx, const Graph &g) {
+    if (ctx->params.bfs_prune == 0 || (ctx->params.bfs_prune == 2 && g.V < 4096)) return true;
+    const PruneDecision *d = g.and_key.empty()
+                                 ? &g.pdec
+                                 : (ctx->and_pdec.count(g.and_key) ? &ctx->and_pdec[g.and_key] : nullptr);
+    return d && d->valid && !d->active;
+}
 void closeness_group(hm_ctx *ctx, const std::vector<Graph *> &gs) {
     int64_t Vs = 0;
     for (const Graph *g : gs) Vs += g->V;
     const int f = ctx->params.bfs_fuse;
-    const bool fuse = gs.size() > 1 && (f == 1 || (f == 2 && Vs <= FUSE_AUTO_MAX_V));
-    if (fuse) {
+    if (gs.size() > 1 && (f == 1 || (f == 2 && Vs <= FUSE_AUTO_MAX_V))) {
         closeness_multi(ctx, gs);
         return;
     }
-    for (Graph *g : gs) closeness_multi(ctx, std::vector<Graph *>{g});
+    std::vector<Graph *> grp;                      // f == 2: groups of known-unpruned graphs
+    int64_t gv = 0;
+    auto flush = [&]() {
+        if (grp.size() > 1) closeness_multi(ctx, grp);
+        else if (grp.size() == 1) closeness_multi(ctx, std::vector<Graph *>{grp[0]});
+        grp.clear();
+        gv = 0;
+    };
+    for (Graph *g : gs) {
+        if (f == 2 && g->V < FUSE_AUTO_MAX_V && known_unpruned(ctx, *g)) {
+            if (gv + g->V > FUSE_AUTO_MAX_V) flush();
+            grp.push_back(g);
+            gv += g->V;
+        } else {
+            closeness_multi(ctx, std::vector<Graph *>{g});
+        }
+    }
+    flush();
 }
 
 void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out) {
@@ -930,6 +955,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         ctx->params.bfs_blocks_per_sm != 1)
         W = V <= 1024 ? 16 : V <= 2048 ? 32 : 64;
 
+    bool t_ordered = false;               // the pruned core relabelled in T order (k_vert_keys)
     Buf parent((size_t)V * 4, s), label((size_t)V * 4, s), csize((size_t)V * 4, s);
     Buf key1((size_t)V * 8, s), key2((size_t)V * 8, s);
     Buf size_s((size_t)V * 4, s), cstart((size_t)V * 4, s), rank((size_t)V * 4, s);
@@ -1047,8 +1073,13 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     count_launch(ctx);
     {
         const int kbits = sh;                                      // keys <= V
-        // pruned graphs: vertex keys carry the core's T order in 8 more bits (k_vert_keys)
-        const int kshift = (pr.active && sh + 8 <= 32) ? 8 : 0;
+        // pruned graphs: vertex keys carry the core's T order in 8 more bits (k_vert_keys) -- only without
+        // hub rows: on R-MAT layers the large hanging trees hang off the hubs, and T order packs the hubs
+        // into the first groups and source windows (C4's pruned layers 25.7 -> 30.6 ms with it)
+        const int to = ctx->params.bfs_torder;
+        const int kshift = (pr.active && sh + 8 <= 32 &&
+                            (to == 2 || (to == 1 && pr.shape_known && pr.maxdeg <= 256))) ? 8 : 0;
+        t_ordered = kshift != 0;
         size_t tb = 0;
         HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, V, 0, kbits + kshift, s));
         size_t tb2 = 0;
@@ -1225,13 +1256,13 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     if (pr.active) {                    // weights 1 + T(s) of the pruned MS-BFS (prune.cu (1))
         Trow.alloc((size_t)V * 4, s);
         planes.alloc((size_t)BFS_T_BITS * W * 8, s);
-        tconst.alloc((size_t)(W / 2) * 4 + 16, s);
+        if (t_ordered) tconst.alloc((size_t)(W / 2) * 4 + 16, s);
         k_row_T<<<gb, TB, 0, s>>>(n2o.as<int32_t>(), pr.tsz.as<uint32_t>(), scalars, Trow.as<uint32_t>());
         check_launch("k_row_T");
         count_launch(ctx);
         a.tw = Trow.as<uint32_t>();
         a.planes = planes.as<unsigned long long>();
-        a.tconst = tconst.as<int32_t>();
+        a.tconst = t_ordered ? tconst.as<int32_t>() : nullptr;
     }
     a.shard = shard;
     a.nshards = nshards;

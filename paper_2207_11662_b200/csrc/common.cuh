@@ -117,6 +117,7 @@ struct Params {
     int bfs_fuse = 2;          // hm_closeness_multi: 0 one pass per graph, 1 one fused pass, 2 (auto) fused when
                                // sum of V <= 2^17 (small graphs that cannot fill the GPU alone)
     int bfs_count_rows = 0;    // MS-BFS: 1 = counting instantiation (hm_stats bfs_gathers / bfs_own_reads)
+    int bfs_torder = 1;        // pruned core rows in T order: 0 never, 1 graphs without hub rows, 2 always
     int topk_tiles = 1;        // top-K: 1 two-phase tile select (one launch) where it fits, 0 cooperative radix select
     int bfs_td = 0;            // direction switch: top-down levels when frontier * bfs_td <= rows (0 = off)
     int timing = 0;

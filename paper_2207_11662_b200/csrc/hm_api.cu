@@ -139,6 +139,9 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         ctx->params.bfs_prune = (int)value;
     } else if (n == "bfs_count_rows") {
         ctx->params.bfs_count_rows = value ? 1 : 0;
+    } else if (n == "bfs_torder") {
+        HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_torder must be 0, 1 or 2");
+        ctx->params.bfs_torder = (int)value;
     } else if (n == "topk_tiles") {
         ctx->params.topk_tiles = value ? 1 : 0;
     } else if (n == "bfs_fuse") {

@@ -475,7 +475,10 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
 // HV: heavy-row path compiled in (false only for graphs without heavy rows: a leaner kernel)
 // CNT: count the row traffic (gathered rows, own rows read) into counters[8..9] -- a separate
 // instantiation, so the timed kernels carry none of it (it costs them ~3 %)
-template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, bool CNT = false,
+// TC (with WT): the pruned core is in T order (closeness.cu k_vert_keys) -- chunks of one T are weighed by
+// T x popc, the others by the planes; a separate instantiation, so graphs without T order run the plain
+// plane code
+template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, bool CNT = false, bool TC = false,
           int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
 __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     constexpr int T = W / 2 < 32 ? W / 2 : 32;   // lanes per row in the heavy path (W <= 64 with heavy rows)
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     __shared__ Smem<BLOCK / 32> sm;
     __shared__ unsigned long long s_pl[WT ? BFS_T_BITS : 1][WT ? W : 1];   // T bit planes of the batch window
     __shared__ int s_nb;
-    __shared__ int s_tc[WT ? W / 2 : 1];   // T of each 128-source chunk of the window when constant, else -1
+    __shared__ int s_tc[TC ? W / 2 : 1];   // T of each 128-source chunk of the window when constant, else -1
 #ifdef HM_MSBFS_PROF
     __shared__ int s_tmin, s_tmax;
 #endif
@@ -588,6 +591,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
             // chunks of 128 sources (words 2c, 2c+1) with one T: the core rows are sorted by T (k_vert_keys),
             // so nearly all are, and a commit weighs them by T x popc instead of the planes
+            if (TC)
             for (int64_t c = gwarp; c < W / 2; c += nwarps) {
                 unsigned tmin = 0xffffffffu, tmax = 0u;
 #pragma unroll
@@ -624,7 +628,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 s_pl[i / W][i % W] = x;
                 if (x) atomicMax(&s_nb, i / W + 1);
             }
-            for (int i = threadIdx.x; i < W / 2; i += BLOCK) s_tc[i] = a.tconst[i];
+            if (TC)
+                for (int i = threadIdx.x; i < W / 2; i += BLOCK) s_tc[i] = a.tconst[i];
             __syncthreads();
         }
 
@@ -878,7 +883,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                             // chunks of one T: T x popc; the others by T's bit planes (rows without new
                             // sources skip both: cnt is team-uniform here)
                             int needp = 0;
-                            if (has && cnt && v < n_giant) {
+                            if (TC && has && cnt && v < n_giant) {
         #pragma unroll
                                 for (int q = 0; q < VEC; ++q) {
                                     const int t = s_tc[q * TL + ltl];
@@ -886,14 +891,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                                     else needp = 1;
                                 }
                             }
-                            const int nbp = needp ? s_nb : 0;
+                            const int nbp = (TC ? needp : (has && cnt && v < n_giant)) ? s_nb : 0;
                             const int nbw = __reduce_max_sync(FULL, (unsigned)nbp);   // warp-uniform trip count
                             for (int b = 0; b < nbw; ++b) {
                                 unsigned c2 = 0;
         #pragma unroll
                                 for (int q = 0; q < VEC; ++q) {
                                     const int wi = 2 * (q * TL + ltl);
-                                    if (s_tc[q * TL + ltl] < 0)
+                                    if (!TC || s_tc[q * TL + ltl] < 0)
                                         c2 += __popcll(acc[q].x & s_pl[b][wi]) + __popcll(acc[q].y & s_pl[b][wi + 1]);
                                 }
                                 if (b < nbp) wsum += (unsigned long long)c2 << b;
@@ -1065,6 +1070,9 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
             else
                 kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false, true>
                             : (const void *)msbfs_kernel<64, 16, 4, 2, false, false, true>;
+        } else if (a.tw && a.tconst) {                         // weighted, T-ordered core
+            kern = a.hstart ? (const void *)msbfs_kernel<64, 16, 4, 2, true, true, false, true>
+                            : (const void *)msbfs_kernel<64, 16, 4, 2, true, false, false, true>;
         } else if (a.hstart)
             kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true> : (const void *)msbfs_kernel<64, 16, 4, 2, false>;
         else
@@ -1078,6 +1086,8 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         if (a.count_rows)
             kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false, true>
                         : (const void *)msbfs_kernel<128, 16, 2, 2, false, false, true>;
+        else if (a.tw && a.tconst)
+            kern = (const void *)msbfs_kernel<128, 16, 2, 2, true, false, false, true>;
         else
             kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false>
                         : (const void *)msbfs_kernel<128, 16, 2, 2, false, false>;

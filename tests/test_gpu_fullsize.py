@@ -71,15 +71,15 @@ def check_graph(ctx, g, V, want, what):
 
 
 KNOBS = {"default": {}, "noprune-w32-contig": {"bfs_prune": 0, "bfs_interleave": 0, "bfs_words": 32},
-         "separate": {"bfs_fuse": 0}, "fused": {"bfs_fuse": 1}}
+         "separate": {"bfs_fuse": 0}, "fused": {"bfs_fuse": 1}, "torder2": {"bfs_torder": 2}}
 
 
 @pytest.mark.parametrize("name,knobs", [("C1", "default"), ("C2", "default"), ("C3", "default"),
                                         ("C4", "default"), ("C5", "default"),
                                         ("C4", "noprune-w32-contig"), ("C5", "noprune-w32-contig"),
-                                        ("C2", "separate"), ("C3", "fused"), ("C1", "fused")],
+                                        ("C2", "separate"), ("C3", "fused"), ("C1", "fused"), ("C4", "torder2")],
                          ids=["C1", "C2", "C3", "C4", "C5", "C4-noprune-w32", "C5-noprune-w32",
-                              "C2-separate", "C3-fused", "C1-fused"])
+                              "C2-separate", "C3-fused", "C1-fused", "C4-torder2"])
 def test_fullsize_config(Context, name, knobs):
     import torch
     gold = golden(name)

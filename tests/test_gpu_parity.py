@@ -521,6 +521,30 @@ def test_closeness_multi_fused(hm, name, V, fuse):
             check_psi(h.V, O.and_aggregate([Es[i] for i in T]), fused[g])
 
 
+def test_closeness_multi_groups_unpruned(hm):
+    """automatic fusing above 2^17 vertices: graphs whose cached pruning decision is "unpruned" are fused
+    in groups of <= 2^17 vertices, pruned ones run alone; every result equals one pass per graph."""
+    h = build_config("C3", V=40000)
+    with hm() as ctx:
+        ids, _ = ctx.load_layers(h.V, h.layers)
+        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        gids = list(ids) + ands
+        ctx.set_param("bfs_fuse", 0)
+        ctx.closeness_multi(gids)                      # caches every graph's pruning decision
+        sep = {g: ctx.closeness_results(g) for g in gids}
+        ctx.set_param("bfs_fuse", 2)
+        ctx.sync()
+        ctx.stats(reset=True)
+        ctx.closeness_multi(gids)
+        st = ctx.stats(reset=True)
+        assert st["host_syncs"] == 0
+        assert st["bfs_launches"] < len(gids)          # the ER layers share a pass
+        for g in gids:
+            got = ctx.closeness_results(g)
+            for key in ("S", "k", "c", "pen"):
+                assert np.array_equal(got[key], sep[g][key]), (g, key)
+
+
 # ---------------------------------------------------------------------------
 # Sharded Psi (SURVEY §8(f) rank 4): partial sums over source-batch shards add up
 # to S exactly, and finalising from the sum reproduces every cached result
@@ -605,7 +629,7 @@ def test_random_sweep_all_knobs(hm):
     rng = random.Random(20220722)
     knobs = dict(bfs_words=[0, 8, 16, 32, 64, 128], bfs_prune=[0, 1, 2], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
                  bfs_chg_smem=[0, 1], bfs_unit=[0, 2, 4, 8, 16, 32], bfs_heavy=[0, 2, 16, 256], bfs_blocks_per_sm=[0, 1],
-                 bfs_fbar=[0, 1], cc_init=[0, 1, 2, 3, 4], bfs_td=[0, 2, 8, 32, 1 << 20])
+                 bfs_fbar=[0, 1], cc_init=[0, 1, 2, 3, 4], bfs_td=[0, 2, 8, 32, 1 << 20], bfs_torder=[0, 1, 2])
     with hm() as ctx:
         for t in range(200):
             V, E = _shape(rng, t)
