@@ -101,6 +101,7 @@ __device__ __forceinline__ int ld_cs(const int32_t *p) {   // arcs: read once pe
 // arcs kept L2-resident (HM_CSR_POLICY 1, default: evict_last hint; the CSR is read every level -- C5 layer
 // 65.3 -> 65.0 ms, C4 layer 1 25.9 -> 24.8 ms against the streaming .cs load)
 __device__ __forceinline__ int ld_pol(const int32_t *p, uint64_t pol) {
+    if (!pol) return ld_cs(p);                      // no L2 policies (bfs_hints without bit 1)
     int v;
     asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
