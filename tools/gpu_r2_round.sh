@@ -28,7 +28,22 @@ P="python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-e2e
 $P > gpurun_out/plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:msbfs -c ${NCU_C:-4} -o gpurun_out/msbfs_full_$CFG -f $P > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
-for k in 0 3; do python tools/ncu_summary.py gpurun_out/msbfs_full_$CFG.ncu-rep $k > gpurun_out/ncu_summary_${CFG}_$k.txt 2>&1; done
+python tools/ncu_summary.py gpurun_out/msbfs_full_$CFG.ncu-rep 0 > gpurun_out/ncu_summary_${CFG}_0.txt 2>&1
+# the AND launch alone (its replay inside the 4-launch capture reports no metrics)
+cat > /tmp/and_only.py <<'PY'
+import sys; sys.path.insert(0, ".")
+from paper_2207_11662_b200 import Context
+from synth import build_config
+h = build_config(sys.argv[1])
+with Context(0) as ctx:
+    ctx.load_layers(h.V, h.layers)
+    g = ctx.and_aggregate(list(h.subsets[0]))
+    ctx.closeness(g, out={})
+    ctx.sync()
+PY
+python /tmp/and_only.py $CFG && ncu --set full --clock-control none --import-source on -k regex:msbfs -c 1 \
+  -o gpurun_out/msbfs_full_and_$CFG -f python /tmp/and_only.py $CFG > gpurun_out/ncu_and.log 2>&1
+python tools/ncu_summary.py gpurun_out/msbfs_full_and_$CFG.ncu-rep 0 > gpurun_out/ncu_summary_${CFG}_3.txt 2>&1
 python tools/launch_summary.py gpurun_out/launches_$CFG.csv > gpurun_out/launch_summary_$CFG.txt 2>&1
 # source-batch sharding at N = 1 (the partial/combine split's own cost)
 timeout 900 python bench.py --config $CFG --shard --no-cpu-baseline --no-e2e > gpurun_out/bench_shard_$CFG.log 2>&1; echo "shard rc=$?"
