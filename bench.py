@@ -513,7 +513,7 @@ def run_ours(args, rank, world, local_rank):
         dom_ms = step_fused["ms"] / max(1, step_fused["launches"])
         dom_bytes = step_fused["model_bytes"] / max(1, step_fused["launches"])
         dom_traffic = None
-        dom_name = "msbfs_kernel, the step's fused launch over all its graphs (bfs_fuse)"
+        dom_name = "msbfs_kernel, the step's own launches (graphs fused by bfs_fuse), averaged"
     elif layer_e:
         dom_ms = float(np.mean([v["ms"] for v in layer_e]))
         dom_bytes = float(np.mean([v["model_bytes"] for v in layer_e]))
@@ -547,7 +547,9 @@ def run_ours(args, rank, world, local_rank):
             "l2_row_traffic": l2_roof,
             "levels_per_launch": levels_per_launch, "bfs_ms_per_launch_all": bfs_ms_avg,
             "bfs_share_of_step": bfs_ms_step / max(ms_per_step, 1e-9),
-            "fused_graphs": n_graphs_step if fused_step else 1, "step_fused_launch": step_fused}
+            "fused_graphs": n_graphs_step if (fused_step and probe["bfs_launches"] == 1) else 1,
+            "bfs_launches_per_step": probe["bfs_launches"], "graphs_per_step": n_graphs_step,
+            "step_fused_launch": step_fused}
 
     line = {
         "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",
