@@ -470,31 +470,54 @@ def run_ours(args, rank, world, local_rank):
             per_graph[name] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
         for g in ands:
             ctx.free_graph(g)
-    step_fused = None
-    if fused_step and not args.shard:
-        # the step's own fused MS-BFS launch (one eager Psi over all graphs of the step)
+    # ---- the step's own MS-BFS launches (the library fuses graphs, bfs_fuse): measured per part of the
+    # step's Psi -- everything when the whole step is one launch (C1, C2), else the layers' Psi (one fused
+    # launch on C5) and the AND graphs' Psi -- one counting run (row traffic), one timed run
+    step_parts = {}
+
+    def measure_part(name, gids_of):
         ctx.sync()
         ctx.stats(reset=True)
-        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        ands_ = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        ids_ = gids_of(ands_)
+        ctx.set_param("bfs_count_rows", 1)
+        psi(ids_)
+        ctx.sync()
+        sc = ctx.stats(reset=True)
+        ctx.set_param("bfs_count_rows", 0)
         flush_l2()
-        psi(list(range(len(h.layers))) + ands)
+        psi(ids_)
         ctx.sync()
         sg = ctx.stats(reset=True)
+        for g in ands_:
+            ctx.free_graph(g)
         t = sg["bfs_ms"] / 1e3
         model = sg["bfs_model_bytes"]
         comp = sg["bfs_state_bytes"] + sg["bfs_csr_bytes"]
-        step_fused = {"graphs": n_graphs_step, "launches": sg["bfs_launches"], "ms": round(sg["bfs_ms"], 4),
-                      "levels": sg["bfs_levels"], "batches": sg["bfs_batches"], "model_bytes": model,
-                      "compulsory_bytes": comp, "row_commits": sg["bfs_row_commits"],
-                      "model_frac": round(model / t / 1e9 / peak_gbs, 4) if t > 0 else None,
-                      "compulsory_frac": round(comp / t / 1e9 / peak_gbs, 4) if t > 0 else None}
-        for g in ands:
-            ctx.free_graph(g)
-    if step_fused:                          # headline: the fused launch the step runs
-        n_bfs = step_fused["launches"]
-        bfs_ms_avg = step_fused["ms"] / max(1, n_bfs)
-        levels_per_launch = step_fused["levels"] / max(1, n_bfs)
-        bfs_ms_step = step_fused["ms"]
+        rsz = sc["bfs_state_bytes"] / (2 * sc["bfs_row_commits"]) if sc["bfs_row_commits"] else 0.0
+        rowb = rsz * (sc["bfs_gathers"] + sc["bfs_own_reads"] + sc["bfs_row_commits"])
+        step_parts[name] = {
+            "graphs": len(ids_), "launches": sg["bfs_launches"], "ms": round(sg["bfs_ms"], 4),
+            "levels": sg["bfs_levels"], "batches": sg["bfs_batches"], "model_bytes": model,
+            "compulsory_bytes": comp, "row_commits": sg["bfs_row_commits"],
+            "gathers": sc["bfs_gathers"], "own_reads": sc["bfs_own_reads"], "row_traffic_bytes": rowb,
+            "model_frac": round(model / t / 1e9 / peak_gbs, 4) if t > 0 else None,
+            "compulsory_frac": round(comp / t / 1e9 / peak_gbs, 4) if t > 0 else None,
+            "row_traffic_frac_l2": round(rowb / t / 1e9 / l2_peak, 4) if (t > 0 and l2_peak) else None}
+
+    nl = len(h.layers)
+    if fused_step and not args.shard:
+        if probe["bfs_launches"] == 1:
+            measure_part("step", lambda ands_: list(range(nl)) + ands_)
+        else:
+            measure_part("layers", lambda ands_: list(range(nl)))
+            measure_part("ands", lambda ands_: ands_)
+    step_fused = step_parts.get("step") or step_parts.get("layers")
+    if step_parts:                          # the step's own launches
+        n_bfs = sum(v["launches"] for v in step_parts.values())
+        bfs_ms_step = sum(v["ms"] for v in step_parts.values())
+        bfs_ms_avg = bfs_ms_step / max(1, n_bfs)
+        levels_per_launch = sum(v["levels"] for v in step_parts.values()) / max(1, n_bfs)
     elif per_graph:                         # per-launch numbers from the eager per-graph pass
         n_bfs = len(per_graph)
         bfs_ms_avg = float(np.mean([v["ms"] for v in per_graph.values()]))
@@ -505,22 +528,27 @@ def run_ours(args, rank, world, local_rank):
         bfs_ms_avg = st["bfs_ms"] / n_bfs
         levels_per_launch = st["bfs_levels"] / n_bfs
         bfs_ms_step = st["bfs_ms"] / args.steps
-    # headline: the dominant kernel, the plain MS-BFS launches of the layers (3 of the 4 launches of a
-    # C5 step, ~75 % of it); algorithmic bytes = SURVEY §8(d) dense-level model of this algorithm,
-    # accumulated by the kernel per batch:  L * (4 (rows + 1) + 4 arcs + 2 R rows),  R = 8 W bytes
+    # headline: the dominant kernel -- the layers' MS-BFS (3 of the 4 graphs of a C5 step, one fused launch,
+    # ~80 % of the step; the whole step's launch on C1 / C2); algorithmic bytes = SURVEY §8(d) dense-level
+    # model of this algorithm, accumulated by the kernel per batch:  L * (4 (rows + 1) + 4 arcs + 2 R rows),
+    # R = 8 W bytes
     layer_e = [v for k, v in per_graph.items() if k.startswith("L")]
+    dom_rowb = None
     if step_fused:
         dom_ms = step_fused["ms"] / max(1, step_fused["launches"])
         dom_bytes = step_fused["model_bytes"] / max(1, step_fused["launches"])
+        dom_rowb = step_fused["row_traffic_bytes"] / max(1, step_fused["launches"])
         dom_traffic = None
-        dom_name = "msbfs_kernel, the step's own launches (graphs fused by bfs_fuse), averaged"
+        dom_name = ("msbfs_kernel, the step's one launch over all its graphs (bfs_fuse)" if "step" in step_parts
+                    else "msbfs_kernel, the layers' launch(es) of the step (graphs fused by bfs_fuse), per launch")
     elif layer_e:
         dom_ms = float(np.mean([v["ms"] for v in layer_e]))
         dom_bytes = float(np.mean([v["model_bytes"] for v in layer_e]))
+        dom_rowb = float(np.mean([v["row_traffic_bytes"] for v in layer_e]))
         dom_traffic = (float(np.mean([v["ncu_dram_bytes"] for v in layer_e]))
                        if all("ncu_dram_bytes" in v for v in layer_e) else None)
         dom_name = "msbfs_kernel (plain instantiation), the layer launches"
-    else:                                   # --shard / --fused: all launches together
+    else:                                   # --shard: all launches together
         dom_ms = bfs_ms_avg
         dom_bytes = st["bfs_model_bytes"] / n_bfs
         dom_traffic = None
@@ -529,8 +557,8 @@ def run_ours(args, rank, world, local_rank):
     # the bound the dense levels actually meet: row traffic through L2 (gathered rows, own rows read, rows
     # written; counted by the kernel) against the same pattern's measured ceiling (no BFS logic)
     l2_roof = None
-    if layer_e and l2_peak and all(v.get("row_traffic_bytes") for v in layer_e) and not step_fused:
-        rb = float(np.mean([v["row_traffic_bytes"] for v in layer_e]))
+    if dom_rowb and l2_peak and dom_ms > 0:
+        rb = dom_rowb
         l2a = rb / (dom_ms / 1e3) / 1e9
         l2_roof = {"bound": "l2", "achieved": l2a, "peak": l2_peak, "unit": "GB/s", "frac": l2a / l2_peak,
                    "bytes_per_launch": rb, "peak_source": l2_src,
@@ -549,7 +577,7 @@ def run_ours(args, rank, world, local_rank):
             "bfs_share_of_step": bfs_ms_step / max(ms_per_step, 1e-9),
             "fused_graphs": n_graphs_step if (fused_step and probe["bfs_launches"] == 1) else 1,
             "bfs_launches_per_step": probe["bfs_launches"], "graphs_per_step": n_graphs_step,
-            "step_fused_launch": step_fused}
+            "step_launches": step_parts}
 
     line = {
         "metric": "all-sources BFS closeness TEPS (HoMLN) on 1 B200; also s/HoMLN and % HBM roofline",

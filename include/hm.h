@@ -89,7 +89,7 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   bottom-up over every row not yet complete; 0 = always bottom-up
  *   "bfs_fuse"    : hm_closeness_multi: 0 one pass per graph, 1 one fused pass over the disjoint union,
  *                   2 (default) fused when sum of V <= 2^17 (graphs too small to fill the GPU alone), else
- *                   graphs known to run unpruned fused in groups of <= 2^17 vertices, the rest one pass each
+ *                   graphs known to run unpruned fused in groups of <= 2^20 vertices, the rest one pass each
  *   "bfs_count_rows": 1 runs the default MS-BFS kernels in a counting instantiation that fills hm_stats
  *                   bfs_gathers / bfs_own_reads (the row traffic; ~3 % slower), 0 (default) the timed ones
  *   "bfs_torder"  : pruned graphs: relabel the pruned core in order of hanging-tree size T so the MS-BFS weighs
@@ -166,7 +166,7 @@ hm_status hm_closeness(hm_ctx *ctx, int32_t g, uint64_t *dist_sum, int32_t *reac
  * their all-sources BFS runs over the disjoint union in ONE pass and shares
  * every level step (no pruning, no host round trip); otherwise (default) the
  * graphs known not to be pruned (an earlier call's cached decision) are fused
- * in groups of <= 2^17 vertices and every other graph gets its own
+ * in groups of <= 2^20 vertices and every other graph gets its own
  * hm_closeness pass.  Results are per graph, identical to n separate hm_closeness
  * calls either way, cached for hm_compose / hm_topk_closeness / hm_cc_nodes and
  * readable with hm_closeness_results.  graph_ids: host array.  Errors: n < 1 or

@@ -824,9 +824,11 @@ void closeness(hm_ctx *ctx, Graph &G) { closeness_multi(ctx, std::vector<Graph *
 // small-path passes, 0.42 ms fused).  Larger graphs fill the grid on their own and keep their own
 // pruning (the fused pass does not prune): C3's 14 graphs fused take 57.8 ms, separately 39.9.  Among
 // them, graphs whose (cached) pruning decision is "no pruning" still gain from sharing level steps in
-// groups of <= 2^17 vertices (C3's two ER layers: 17.4 -> 13.6 ms fused), while pruned ones lose
-// (C3's R-MAT layers 6.8 -> 8.8, C4's layers 48.7 -> 65.0) and run one pass each.
+// groups of <= 2^20 vertices (C3's two ER layers: 17.4 -> 13.6 ms fused; C5's three layers: 195.9 ->
+// 189.0 ms), while pruned ones lose (C3's R-MAT layers 6.8 -> 8.8, C4's layers 48.7 -> 65.0) and run
+// one pass each.
 constexpr int64_t FUSE_AUTO_MAX_V = (int64_t)1 << 17;
+constexpr int64_t FUSE_GROUP_MAX_V = (int64_t)1 << 20;
 static bool known_unpruned(hm_ctx *ctx, const Graph &g) {
     if (ctx->params.bfs_prune == 0 || (ctx->params.bfs_prune == 2 && g.V < 4096)) return true;
     const PruneDecision *d = g.and_key.empty()
@@ -851,8 +853,8 @@ void closeness_group(hm_ctx *ctx, const std::vector<Graph *> &gs) {
         gv = 0;
     };
     for (Graph *g : gs) {
-        if (f == 2 && g->V < FUSE_AUTO_MAX_V && known_unpruned(ctx, *g)) {
-            if (gv + g->V > FUSE_AUTO_MAX_V) flush();
+        if (f == 2 && g->V < FUSE_GROUP_MAX_V && known_unpruned(ctx, *g)) {
+            if (gv + g->V > FUSE_GROUP_MAX_V) flush();
             grp.push_back(g);
             gv += g->V;
         } else {
@@ -1049,6 +1051,31 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr, dec);
     }
     rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
+    if (gs.size() > 1) {
+        // a fused union's shape from its graphs' cached pruning decisions (all known: the automatic
+        // grouping fuses only such graphs) -- the batch width and the lean kernel choice below
+        bool all = true;
+        int maxdeg = 0;
+        int64_t arcs = 0, nonisol = 0;
+        for (const Graph *g : gs) {
+            const PruneDecision *d = g->and_key.empty()
+                                         ? &g->pdec
+                                         : (ctx->and_pdec.count(g->and_key) ? &ctx->and_pdec[g->and_key] : nullptr);
+            if (!d || !d->valid) {
+                all = false;
+                break;
+            }
+            maxdeg = d->maxdeg > maxdeg ? d->maxdeg : maxdeg;
+            arcs += d->arcs;
+            nonisol += d->nonisolated;
+        }
+        if (all) {
+            pr.shape_known = true;
+            pr.maxdeg = maxdeg;
+            pr.arcs = arcs;
+            pr.nonisolated = (int)nonisol;
+        }
+    }
     phase_end(ctx, PH_PRUNE, ph);
     ph = phase_begin(ctx);
 
@@ -1151,9 +1178,11 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     // graphs (many isolated vertices) need far less than V rows of state
     int64_t frows = V;
     int32_t h_heavy = 0;
-    // small graphs (<= 256 MB of visited-set rows at V rows) skip the row count and its host round trip:
-    // F is sized for V rows and the heavy-row arrays for the bound nnz / (heavy_deg + 1)
-    const bool count_rows = (int64_t)V * (int64_t)rowb * 2 > ((int64_t)256 << 20);
+    // graphs of <= 256 MB of visited-set rows at V rows -- or <= 4 GB when the graph's shape is known from its
+    // (cached) pruning decision, e.g. a fused group of C5's layers -- skip the row count and its host round
+    // trip: F is sized for V rows and the heavy-row arrays for the bound nnz / (heavy_deg + 1)
+    const int64_t state_bytes = (int64_t)V * (int64_t)rowb * 2;
+    const bool count_rows = state_bytes > ((int64_t)4 << 30) || (!pr.shape_known && state_bytes > ((int64_t)256 << 20));
     if (!count_rows) {
         if (frows < 32) frows = 32;                                  // as the counted path
         const int64_t bound = U.nnz / ((int64_t)heavy_min + 1);
