@@ -538,7 +538,9 @@ def run_ours(args, rank, world, local_rank):
         dom_ms = step_fused["ms"] / max(1, step_fused["launches"])
         dom_bytes = step_fused["model_bytes"] / max(1, step_fused["launches"])
         dom_rowb = step_fused["row_traffic_bytes"] / max(1, step_fused["launches"])
-        dom_traffic = None
+        # ncu DRAM bytes of the step's layers launch (a steady-state capture, when it matches this build)
+        sl = (traffic or {}).get("step_launches", {}).get("layers")
+        dom_traffic = sl["dram_bytes"] if (sl and "layers" in step_parts and step_parts["layers"]["launches"] == 1) else None
         dom_name = ("msbfs_kernel, the step's one launch over all its graphs (bfs_fuse)" if "step" in step_parts
                     else "msbfs_kernel, the layers' launch(es) of the step (graphs fused by bfs_fuse), per launch")
     elif layer_e:

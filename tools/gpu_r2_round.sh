@@ -12,7 +12,13 @@ $P > gpurun_out/plain3.log 2>&1 && \
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none \
       -k regex:msbfs -c ${NCU_C:-4} -o gpurun_out/msbfs_traffic -f $P > gpurun_out/ncu_traffic.log 2>&1
 echo "ncu traffic rc=$?"
-python tools/ncu_traffic.py gpurun_out/msbfs_traffic.ncu-rep gpurun_out/r2_msbfs_traffic_$CFG.json $CFG 0 11 && \
+# the step's own launches in steady state (second setup step: graphs fused by bfs_fuse)
+NG=$(python -c "from synth import build_config as b; h=b('$CFG'); print(len(h.layers)+len(h.subsets))")
+$P > /dev/null 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none \
+      -k regex:msbfs -s $NG -c 2 -o gpurun_out/msbfs_traffic_step -f $P > gpurun_out/ncu_traffic_step.log 2>&1
+python tools/ncu_traffic.py gpurun_out/msbfs_traffic.ncu-rep gpurun_out/r2_msbfs_traffic_$CFG.json $CFG 0 11 \
+    gpurun_out/msbfs_traffic_step.ncu-rep && \
   cp gpurun_out/r2_msbfs_traffic_$CFG.json profiles/
 timeout 900 python bench.py --config $CFG ${BENCH_ARGS} > gpurun_out/bench_$CFG.log 2>&1; echo "bench rc=$?"
 tail -1 gpurun_out/bench_$CFG.log | cut -c1-600

@@ -1,17 +1,8 @@
-for cap in 0 4 100; do
-HM_DEFINES="HM_PLANE_CAP=$cap" python -m paper_2207_11662_b200.build --force > gpurun_out/build.log 2>&1 || exit 1
-python - <<'PY'
-import sys; sys.path.insert(0, '.')
-from paper_2207_11662_b200 import Context
-from synth import build_config
-h = build_config("C5")
-with Context(0) as ctx:
-    ctx.set_param("timing", 1)
-    ctx.load_layers(h.V, h.layers)
-    g = ctx.and_aggregate([0, 1, 2])
-    ctx.closeness(g); ctx.sync(); ctx.stats(reset=True)
-    ctx.closeness(g); ctx.sync(); st = ctx.stats(reset=True)
-    print("AND", {k: st[k] for k in ("bfs_ms", "bfs_levels")})
-PY
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+for c in C5 C3 C1; do
+  timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/b_$c.log 2>&1
+  echo "$c rc=$?"; tail -1 gpurun_out/b_$c.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']
+print(d['ms_per_step'], d['e2e']['ms_per_step'], d['cuda_graph'], r['kernel'], round(r['frac'],3), r['ms_per_launch'], json.dumps(r['l2_row_traffic'])[:200])
+for k,v in r['step_launches'].items(): print(' ', k, v)"
 done
-python -m paper_2207_11662_b200.build --force > /dev/null 2>&1

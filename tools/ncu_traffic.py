@@ -45,6 +45,26 @@ res = {"config": cfg, "bfs_words": words, "bfs_hints": hints, "src_sha": src_dig
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
                  "lts__t_sector_hit_rate.pct --clock-control none (tools/gpu_traffic.sh), the MS-BFS launches of "
                  "bench.py's setup pass (layers, then AND graphs); ncu replays are serialised and cold-cache"}
+# optional: a second capture of the step's own launches in steady state (graphs fused by bfs_fuse), e.g.
+# `-s <graphs> -c 2` on bench.py: the longest launch is the layers' (C5: the three layers fused)
+if len(sys.argv) > 6 and os.path.exists(sys.argv[6]):
+    raw2 = subprocess.run(["ncu", "-i", sys.argv[6], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows2 = list(csv.reader(io.StringIO(raw2)))
+    h2 = next(i for i, r in enumerate(rows2) if "Kernel Name" in r)
+    hdr2, units2 = rows2[h2], rows2[h2 + 1]
+    step = []
+    for r in rows2[h2 + 2:]:
+        d = dict(zip(hdr2, r))
+        if "msbfs" not in d.get("Kernel Name", ""):
+            continue
+        b = sum(float(d[k]) * scale[units2[hdr2.index(k)]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        t = float(d["gpu__time_duration.sum"]) * tscale.get(units2[hdr2.index("gpu__time_duration.sum")], 1e-3)
+        e = {"kernel": d["Kernel Name"], "dram_bytes": b, "duration_s": t, "dram_GBps": b / t / 1e9}
+        if "lts__t_sector_hit_rate.pct" in d:
+            e["l2_hit_pct"] = float(d["lts__t_sector_hit_rate.pct"])
+        step.append(e)
+    if step:
+        res["step_launches"] = {"layers": max(step, key=lambda e: e["duration_s"]), "all": step}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in res.items() if k not in ("per_launch", "per_graph")}))
 for n, p in zip(names, per):
