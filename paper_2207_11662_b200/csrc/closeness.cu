@@ -844,6 +844,18 @@ void closeness_group(hm_ctx *ctx, const std::vector<Graph *> &gs) {
         closeness_multi(ctx, gs);
         return;
     }
+    if (f == 2) {
+        // graphs met for the first time: their pruning decision first (components + peeling + one round trip
+        // each, as their own pass would take), so they can join a fused group in this very call
+        for (Graph *g : gs) {
+            const bool want = ctx->params.bfs_prune == 1 || (ctx->params.bfs_prune == 2 && g->V >= 4096);
+            const PruneDecision *d = g->and_key.empty()
+                                         ? &g->pdec
+                                         : (ctx->and_pdec.count(g->and_key) ? &ctx->and_pdec[g->and_key] : nullptr);
+            if (want && g->V < FUSE_GROUP_MAX_V && !(d && d->valid))
+                closeness_multi(ctx, std::vector<Graph *>{g}, 0, 1, nullptr, nullptr, true);
+        }
+    }
     std::vector<Graph *> grp;                      // f == 2: groups of known-unpruned graphs
     int64_t gv = 0;
     auto flush = [&]() {
@@ -880,8 +892,9 @@ void closeness_combine(hm_ctx *ctx, Graph &G, const uint64_t *d_S_total) {
 // i = shard, shard + nshards, ... and the raw partial sums are written out instead of
 // being finalised; with d_S_total the MS-BFS is skipped and the graph is finalised from
 // the given (summed) sums.  Both are single-graph modes.
+// decide_only: one graph, components and the pruning decision only (cached with the graph), nothing else
 void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int nshards, uint64_t *d_S_partial,
-                     const uint64_t *d_S_total) {
+                     const uint64_t *d_S_total, bool decide_only) {
     cudaStream_t s = ctx->stream;
     HM_REQUIRE(!gs.empty(), HM_EINVAL, "no graphs");
     HM_REQUIRE(nshards >= 1 && shard >= 0 && shard < nshards, HM_EINVAL, "need 0 <= shard < nshards");
@@ -1049,6 +1062,10 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
         Graph &G0 = *gs[0];
         PruneDecision *dec = G0.and_key.empty() ? &G0.pdec : &ctx->and_pdec[G0.and_key];
         prune_component(ctx, U.rp, U.col, label.as<int32_t>(), csize.as<int32_t>(), V, pr, dec);
+    }
+    if (decide_only) {
+        phase_end(ctx, PH_PRUNE, ph);
+        return;
     }
     rem = pr.active ? pr.rem.as<int32_t>() : nullptr;
     if (gs.size() > 1) {

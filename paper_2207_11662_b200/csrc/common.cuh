@@ -217,7 +217,8 @@ void build_csr(hm_ctx *ctx, int32_t V, const int32_t *edges_host_or_dev, int64_t
 void and_or_aggregate(hm_ctx *ctx, const std::vector<Graph *> &in, bool is_and, Graph &out);
 void closeness(hm_ctx *ctx, Graph &G);
 void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard = 0, int nshards = 1,
-                     uint64_t *d_S_partial = nullptr, const uint64_t *d_S_total = nullptr);
+                     uint64_t *d_S_partial = nullptr, const uint64_t *d_S_total = nullptr,
+                     bool decide_only = false);
 void closeness_partial(hm_ctx *ctx, Graph &G, int shard, int nshards, uint64_t *d_S_out);
 // hm_closeness_multi: one fused pass or one pass per graph (Params::bfs_fuse)
 void closeness_group(hm_ctx *ctx, const std::vector<Graph *> &gs);
