@@ -143,7 +143,9 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_torder must be 0, 1 or 2");
         ctx->params.bfs_torder = (int)value;
     } else if (n == "topk_tiles") {
-        ctx->params.topk_tiles = value ? 1 : 0;
+        HM_REQUIRE(value == 0 || value == 1 || value == 1024 || value == 2048 || value == 4096 || value == 8192,
+                   HM_EINVAL, "topk_tiles must be 0, 1 (default tile), 1024, 2048, 4096 or 8192");
+        ctx->params.topk_tiles = (int)value;
     } else if (n == "bfs_fuse") {
         HM_REQUIRE(value >= 0 && value <= 2, HM_EINVAL, "bfs_fuse must be 0, 1 or 2 (auto)");
         ctx->params.bfs_fuse = (int)value;

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t *ok, const u
 // finish (ticket) selects the K smallest of the G*K candidates the same way, sorts them (bitonic) and
 // writes their ids.  One launch instead of a 12-pass cooperative select (C3: 40 top-K lists per step).
 constexpr int TT = 1024;            // threads per block
-constexpr int TILE_E = 8192;        // pairs per phase-A block
+constexpr int TILE_MAX = 8192;      // pairs per phase-A block (at most)
 constexpr int CAND_MAX = 16384;     // candidates phase B holds in shared memory (G * K)
 
 __device__ __forceinline__ bool le_depth(uint64_t k, uint32_t id, uint64_t tk, uint32_t ti, int p) {
@@ -354,7 +354,7 @@ __device__ void block_compact(const uint64_t *sk, const uint32_t *si, int n, con
 
 __global__ void __launch_bounds__(TT) k_topk_tiles(const uint64_t *__restrict__ keys, int n, int K,
                                                   uint64_t *cand_k, uint32_t *cand_i, unsigned *ticket,
-                                                  int32_t *out) {
+                                                  int32_t *out, int TILE_E) {
     extern __shared__ unsigned char smem[];
     __shared__ BlkSel bs;
     __shared__ int s_last;
@@ -465,6 +465,8 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
     }
     {
         // two-phase tile select: one launch, no grid barrier (see k_topk_tiles)
+        // tile: topk_tiles = 1 -> 8192 pairs per block; > 1 -> that many (a power of two, 1024 .. 8192)
+        const int TILE_E = ctx->params.topk_tiles > 1 ? ctx->params.topk_tiles : TILE_MAX;
         const int G = (int)((n + TILE_E - 1) / TILE_E);
         if (ctx->params.topk_tiles && (int64_t)G * K <= CAND_MAX && G <= ctx->num_sms) {
             const int nsm = (n < TILE_E ? n : TILE_E) > G * K ? (n < TILE_E ? n : TILE_E) : G * K;
@@ -475,7 +477,7 @@ void topk(hm_ctx *ctx, const uint64_t *d_keys, int32_t n, int32_t K, int32_t *d_
             unsigned *ticket = reinterpret_cast<unsigned *>(ci + (size_t)(G + 1) * K);
             HM_CUDA(cudaMemsetAsync(ticket, 0, 4, s));
             HM_CUDA(cudaFuncSetAttribute(k_topk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_topk_tiles<<<G, TT, sm, s>>>(d_keys, n, K, ck, ci, ticket, d_ids_out);
+            k_topk_tiles<<<G, TT, sm, s>>>(d_keys, n, K, ck, ci, ticket, d_ids_out, TILE_E);
             check_launch("k_topk_tiles");
             count_launch(ctx, 1);
             return;

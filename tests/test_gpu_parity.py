@@ -545,6 +545,31 @@ def test_closeness_multi_groups_unpruned(hm):
                 assert np.array_equal(got[key], sep[g][key]), (g, key)
 
 
+def test_closeness_multi_fresh_graphs_grouped(hm):
+    """automatic fusing on graphs met for the first time: their pruning decisions are taken first in the
+    same call, the unpruned ones fused; results equal one pass per graph (computed in another context)."""
+    h = build_config("C5", V=65536)
+    with hm() as ref:
+        ids, _ = ref.load_layers(h.V, h.layers)
+        ands = [ref.and_aggregate(list(T)) for T in h.subsets]
+        ref.set_param("bfs_fuse", 0)
+        ref.closeness_multi(list(ids) + ands)
+        want = {g: ref.closeness_results(g) for g in list(ids) + ands}
+    with hm() as ctx:
+        ids, _ = ctx.load_layers(h.V, h.layers)
+        ands = [ctx.and_aggregate(list(T)) for T in h.subsets]
+        gids = list(ids) + ands
+        ctx.sync()
+        ctx.stats(reset=True)
+        ctx.closeness_multi(gids)                      # fresh graphs: decide, then group
+        st = ctx.stats(reset=True)
+        assert st["bfs_launches"] < len(gids)          # the C5 layers (unpruned) share one pass
+        for g in gids:
+            got = ctx.closeness_results(g)
+            for key in ("S", "k", "c", "pen"):
+                assert np.array_equal(got[key], want[g][key]), (g, key)
+
+
 # ---------------------------------------------------------------------------
 # Sharded Psi (SURVEY §8(f) rank 4): partial sums over source-batch shards add up
 # to S exactly, and finalising from the sum reproduces every cached result

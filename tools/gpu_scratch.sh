@@ -1,8 +1,6 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
-for c in C5 C3 C1; do
-  timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/b_$c.log 2>&1
-  echo "$c rc=$?"; tail -1 gpurun_out/b_$c.log | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']
-print(d['ms_per_step'], d['e2e']['ms_per_step'], d['cuda_graph'], r['kernel'], round(r['frac'],3), r['ms_per_launch'], json.dumps(r['l2_row_traffic'])[:200])
-for k,v in r['step_launches'].items(): print(' ', k, v)"
+for t in 1 4096 2048 1024 0; do
+  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --set topk_tiles=$t > gpurun_out/b_C3.log 2>&1
+  echo "C3 topk_tiles=$t rc=$?"; tail -1 gpurun_out/b_C3.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'])"
 done
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "topk" > gpurun_out/t.log 2>&1; echo "topk tests rc=$?"; tail -1 gpurun_out/t.log
