@@ -225,22 +225,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-// 16-byte asynchronous global -> shared copies (LDGSTS), L1 bypassed, optional L2 policy
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, uint64_t pol) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    if (pol)
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "l"(pol)
-                     : "memory");
-    else
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
-
-#ifndef HM_ASYNC_GS
-#define HM_ASYNC_GS 0            // > 0: light-row gathers staged through a shared-memory ring of this many rows
-#endif
 
 template <int W, int TL, int VEC>
 __device__ __forceinline__ void ld_row(ulonglong2 (&r)[VEC], const uint64_t *F, int v, int l, uint64_t pol = 0) {
@@ -522,8 +506,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     const int tib = threadIdx.x / T;
     const int ltl = lane % TL;
     const int lteam = lane / TL;
-    const int ring_off = a.chg_smem ? (a.chg_words >> 2) : 0;     // LDGSTS ring after the bitmap staging
-    (void)ring_off;
 
     const int n_live = a.scalars[0];
     const int n_giant = a.scalars[1];
@@ -841,37 +823,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         ulonglong2 acc[VEC];
                         zero_row<VEC>(acc);
                         PROF_COUNT(pf, 0, 1);
-#if HM_ASYNC_GS > 0
-                        // LDGSTS: up to HM_ASYNC_GS neighbour rows in flight per team without registers;
-                        // each lane stages and reads back only its own 16-B chunks (no warp sync)
-                        {
-                            constexpr int AS = HM_ASYNC_GS;
-                            uint4 *ring = s_dyn + ring_off + (size_t)((wib * LTPW + lteam) * AS) * (TL * VEC);
-                            for (int k0 = kb; k0 < kb + rlen; k0 += AS) {
-                                PROF_COUNT(pf, 1, 1);
-        #pragma unroll
-                                for (int q = 0; q < AS; ++q)
-                                    if (k0 + q < ke) {
-                                        const uint64_t *src = Fc + (size_t)su[k0 + q] * W;
-        #pragma unroll
-                                        for (int c = 0; c < VEC; ++c)
-                                            cp_async16(ring + q * (TL * VEC) + c * TL + ltl, src + 2 * (c * TL + ltl),
-                                                       pol_c);
-                                    }
-                                cp_async_wait_all();
-        #pragma unroll
-                                for (int q = 0; q < AS; ++q)
-                                    if (k0 + q < ke) {
-        #pragma unroll
-                                        for (int c = 0; c < VEC; ++c) {
-                                            const uint4 x = ring[q * (TL * VEC) + c * TL + ltl];
-                                            acc[c].x |= ((unsigned long long)x.y << 32) | x.x;
-                                            acc[c].y |= ((unsigned long long)x.w << 32) | x.z;
-                                        }
-                                    }
-                            }
-                        }
-#else
                         for (int k0 = kb; k0 < kb + rlen; k0 += GD) {
                             PROF_COUNT(pf, 1, 1);
                             ulonglong2 x[GD][VEC];
@@ -883,7 +834,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         #pragma unroll
                             for (int q = 0; q < GD; ++q) or_row<VEC>(acc, x[q]);
                         }
-#endif
                         int cnt = 0;
         #pragma unroll
                         for (int q = 0; q < VEC; ++q) {
@@ -1122,7 +1072,6 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     }
 #undef HM_MSBFS_CASE
     size_t dyn = a.chg_smem ? (size_t)a.chg_words * 4 : 0;
-    if (HM_ASYNC_GS > 0) dyn += (size_t)(block / 32) * (32 / TL) * HM_ASYNC_GS * (TL * vec) * 16;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) return -5;
     int maxb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, block, dyn) != cudaSuccess) return -2;

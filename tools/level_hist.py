@@ -19,11 +19,16 @@ with Context(0) as ctx:
         ctx.set_param(k, int(v))
     ctx.set_param("timing", 1)
     ctx.load_layers(h.V, h.layers)
-    g = ctx.and_aggregate(list(h.subsets[0])) if a.graph == "and" else int(a.graph)
-    ctx.closeness(g, out={})
+    if a.graph == "layers":                    # the layers' Psi as the step runs it (fused when unpruned)
+        gl = list(range(len(h.layers)))
+        run = lambda: ctx.closeness_multi(gl)
+    else:
+        g = ctx.and_aggregate(list(h.subsets[0])) if a.graph == "and" else int(a.graph)
+        run = lambda: ctx.closeness(g, out={})
+    run()
     ctx.sync(); ctx.stats(reset=True)
     ctx.set_param("bfs_dbg", 2 | (a.level << 8))
-    ctx.closeness(g, out={})
+    run()
     ctx.sync()
     st = ctx.stats()
     dc = ctx.debug_counts().astype(np.int64)
