@@ -87,6 +87,13 @@ const char *hm_last_error(const hm_ctx *ctx);
  *                   the frontier (rows changed at the previous level) marks its neighbours as candidates,
  *                   then only candidate rows pull -- when frontier rows * bfs_td <= the batch's rows, else
  *                   bottom-up over every row not yet complete; 0 = always bottom-up
+ *   "bfs_push"    : direction optimisation, push form (the per-source top-down BFS step of PAPER.md:209 on the
+ *                   batch's first, sparse levels): while the (row, source) pairs found at the previous level
+ *                   number <= rows * bfs_push / 4, a level pushes each pair's source bit into its neighbours'
+ *                   visited sets (atomic OR; a first set is a discovery at exactly this distance), then the
+ *                   bit-parallel bottom-up levels take over; 0 = off; -1 (default) = automatic: 8 for graphs
+ *                   run at 8192 sources per batch, else off.  Graphs without heavy rows, default kernel
+ *                   shape.  Results are identical either way.
  *   "bfs_fuse"    : hm_closeness_multi: 0 one pass per graph, 1 one fused pass over the disjoint union,
  *                   2 (default) fused when sum of V <= 2^17 (graphs too small to fill the GPU alone), else
  *                   graphs known to run unpruned fused in groups of <= 2^20 vertices, the rest one pass each

@@ -1315,6 +1315,29 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.interleave = ctx->params.bfs_interleave;
     a.dbg_level = ctx->params.bfs_dbg >> 8;                   // bfs_dbg bits 8.. (profiling builds)
     a.count_rows = ctx->params.bfs_count_rows;
+    // top-down push phase (bfs_push): graphs without heavy rows, default kernels, counting barrier
+    Buf plist0, plist1;
+    a.push_num = 0;
+    a.plist[0] = a.plist[1] = nullptr;
+    a.pcur = nullptr;
+    a.pcap = 0;
+    // automatic (-1): on for the 8192-source batches of sparse graphs (C5 AND launch 44.6 -> 42.9 ms: its first
+    // four levels 242 -> 144 us per batch), off at 4096 (C5 layer 65.0 -> 71.2 ms: a push level of 237 K pairs
+    // costs more than the bottom-up level it replaces, and level 0 writes every row)
+    const int push_par = ctx->params.bfs_push >= 0 ? ctx->params.bfs_push : (W == 128 ? 8 : 0);
+    if (push_par > 0 && h_heavy == 0 && !a.count_rows && ctx->params.bfs_fbar && a.td_div == 0 &&
+        ctx->params.bfs_team == 0 && ctx->params.bfs_gd == 0 && ctx->params.bfs_blocks_per_sm != 1 &&
+        (W == 64 || W == 128)) {
+        const int64_t cap = 2 * ((frows * (int64_t)push_par) / 4) + 64 * (int64_t)W + 1024;
+        if (cap < ((int64_t)1 << 30)) {
+            plist0.alloc((size_t)cap * 8, s);
+            plist1.alloc((size_t)cap * 8, s);
+            a.push_num = push_par;
+            a.plist[0] = plist0.as<unsigned long long>();
+            a.plist[1] = plist1.as<unsigned long long>();
+            a.pcap = (int)cap;
+        }
+    }
     {
         // rows per work unit: bfs_unit, or (0, auto) about a quarter of the live rows per warp of
         // a full grid (2 CTAs x 14 warps per SM), as a power of two in [2, 32], 16 taken as 32.
@@ -1336,6 +1359,7 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.flags = flags.as<int32_t>();
     // fused level barrier: two zeroed counters in the same (zeroed) 128-B flags block
     a.lbar = ctx->params.bfs_fbar ? (unsigned long long *)((char *)flags.p + 64) : nullptr;
+    a.pcur = (unsigned *)((char *)flags.p + 96);                // 3 zeroed list cursors after the barrier counters
     a.counters = ctx->dstats.as<unsigned long long>();
     a.dbgc = nullptr;
     if (ctx->params.bfs_dbg & 2) {

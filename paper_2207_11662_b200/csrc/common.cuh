@@ -120,6 +120,9 @@ struct Params {
     int bfs_torder = 1;        // pruned core rows in T order: 0 never, 1 graphs without hub rows, 2 always
     int topk_tiles = 1;        // top-K: 1 two-phase tile select (one launch) where it fits, 0 cooperative radix select
     int bfs_td = 0;            // direction switch: top-down levels when frontier * bfs_td <= rows (0 = off)
+    int bfs_push = -1;         // top-down push phase: first levels of a batch push (row, source) pairs while the
+                               // pairs number <= rows * bfs_push / 4 (0 = off; -1 = automatic: 8 at 8192 sources
+                               // per batch, else off; lean default kernels only)
     int timing = 0;
     int bfs_dbg = 0;
 };

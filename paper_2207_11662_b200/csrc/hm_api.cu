@@ -170,6 +170,9 @@ hm_status hm_set_param(hm_ctx *ctx, const char *name, int64_t value) {
         HM_REQUIRE(value == 0 || value == 4 || value == 8 || value == 16 || value == 32, HM_EINVAL,
                    "bfs_team must be 0 (default), 4, 8, 16 or 32 (and at most words/2)");
         ctx->params.bfs_team = (int)value;
+    } else if (n == "bfs_push") {
+        HM_REQUIRE(value >= -1 && value <= 4096, HM_EINVAL, "bfs_push must be in [-1, 4096]");
+        ctx->params.bfs_push = (int)value;
     } else if (n == "bfs_td") {
         HM_REQUIRE(value >= 0 && value <= (1 << 20), HM_EINVAL, "bfs_td must be in [0, 2^20]");
         ctx->params.bfs_td = (int)value;

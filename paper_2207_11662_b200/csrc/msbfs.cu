@@ -164,6 +164,9 @@ struct Prof {
 #define HM_HEAVY_GD 8
 #endif
 constexpr int HGD = HM_HEAVY_GD;    // heavy-row gathers in flight per team
+#ifndef HM_PUSH_PU
+#define HM_PUSH_PU 4
+#endif
 
 template <int NWARP>
 struct Smem {
@@ -175,6 +178,9 @@ struct Smem {
     int nchg;                    // rows this CTA changed in the current level
     unsigned ngat, nown;         // rows this CTA gathered / own rows it read in the current level
     long long nlast;             // rows the whole grid changed before the last counting barrier
+    int push, emit;              // push phase: this level pushes pairs / appends the pairs it finds
+    unsigned pn;                 // pairs in the list to read
+    int pt;                      // list-producing levels (level 0s, push levels) run so far
     int32_t su[NWARP][CAP];         // staged neighbour ids
     uint8_t sr[NWARP][CAP];         // staged row index within the group
     int16_t seg[NWARP][34];         // segment starts (+ end sentinel)
@@ -301,6 +307,176 @@ __device__ __noinline__ void td_discover(const int32_t *__restrict__ row_ptr, co
                 }
             }
         }
+    }
+}
+
+// ---- Top-down push phase (bfs_push, PS instantiations: graphs without heavy rows) ----
+// The first levels of a batch are sparse: 64 W sources reach few rows, yet a bottom-up level visits every
+// row.  While the (row, source) pairs found at the previous level are few, a level instead runs the
+// per-source top-down step (the BFS the paper's tool runs once per source) on the batch's bit
+// rows: each pair (v, s) ORs bit s into V(u) of every neighbour u (atomicOr); a first set is the discovery
+// d(s, u) = d, which adds d (x the source's weight) to S(u), 1 to K(u), marks u changed and, while the next
+// level will still push, appends (u, s).  All rows live in buffer F[0] during the phase (level 0 writes
+// every row: zero, the sources' own bit set); the bottom-up levels take over with the buffer parity shifted
+// so that the last push level's rows are the ones gathered.  Sums are integers: the result is identical.
+//
+// thread 0, after a level's barrier: the pairs that level appended (cursor lt % 3) decide whether the next
+// level pushes, and whether it appends what it finds (predicted from the growth of the lists)
+template <class SM>
+__device__ __forceinline__ void push_decide(const BfsArgs &a, SM &sm, int lt, int hi, bool first) {
+    unsigned n;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(a.pcur + lt % 3) : "memory");
+    const bool listed = first || sm.emit;
+    const double lim = (double)hi * (double)a.push_num * 0.25;
+    const bool push = listed && n > 0u && n <= (unsigned)a.pcap && (double)n <= lim;
+    double g = first ? (double)a.row_ptr[hi] / (double)(hi > 0 ? hi : 1) : (double)n / (double)(sm.pn ? sm.pn : 1u);
+    if (g < 1.0) g = 1.0;
+    sm.emit = (push && (double)n * g <= lim) ? 1 : 0;
+    sm.push = push ? 1 : 0;
+    sm.pn = n;
+}
+
+// one push level d over the n pairs of Lr (a warp per 32 pairs, a lane per pair, the arc loop warp-uniform);
+// returns the rows this thread was first to mark changed
+template <int W, bool WT>
+__device__ __noinline__ int push_level(const BfsArgs &a, const unsigned long long *Lr, unsigned n,
+                                       unsigned long long *Lw, unsigned *cur, bool emit, uint32_t *chn,
+                                       int d, int64_t base, int n_giant, int64_t gwarp, int64_t nwarps) {
+    constexpr int64_t B = 64 * W;
+    constexpr int PU = HM_PUSH_PU;                           // row atomics in flight per lane
+    const int lane = threadIdx.x & 31;
+    const unsigned ltmask = (1u << lane) - 1u;
+    uint64_t *Fp = a.F[0];
+    unsigned *K32 = reinterpret_cast<unsigned *>(a.K);
+    int nchg = 0;
+    for (int64_t p0 = gwarp * 32; p0 < (int64_t)n; p0 += nwarps * 32) {
+        const int64_t p = p0 + lane;
+        int v = -1, j = 0, r0 = 0, deg = 0;
+        if (p < (int64_t)n) {
+            const unsigned long long pr = __ldcg(Lr + p);     // written by other CTAs at the previous level
+            v = (int)(pr >> 16);
+            j = (int)(pr & 0xffffull);
+            r0 = a.row_ptr[v];
+            deg = a.row_ptr[v + 1] - r0;
+        }
+        int2 ci = make_int2(0, 0);
+        if (v >= 0) ci = comp_of(a, v, n_giant);
+        int64_t nb = (int64_t)ci.y - base;
+        if (nb > B) nb = B;
+        unsigned long long wt = 1ull;                        // the source's weight 1 + T(s) (pruned core)
+        if constexpr (WT)
+            if (v >= 0 && v < n_giant) wt += (unsigned long long)a.tw[base + j];
+        const unsigned long long bit = 1ull << (j & 63);
+        const int word = j >> 6;
+        const int dmax = __reduce_max_sync(FULL, deg);
+        for (int a0 = 0; a0 < dmax; a0 += PU) {
+            int u[PU];
+            unsigned long long old[PU];
+#pragma unroll
+            for (int q = 0; q < PU; ++q) u[q] = (a0 + q < deg) ? (a.col[r0 + a0 + q] >> 5) : -1;
+#pragma unroll
+            for (int q = 0; q < PU; ++q) {
+                old[q] = bit;
+                if (u[q] >= 0) old[q] = atomicOr(reinterpret_cast<unsigned long long *>(Fp + (size_t)u[q] * W + word), bit);
+            }
+            unsigned bm[PU], ko[PU], co[PU];
+            int tot = 0;
+            // the discoveries' updates are issued together (their returns overlap), then read
+#pragma unroll
+            for (int q = 0; q < PU; ++q) {
+                const bool disc = u[q] >= 0 && !(old[q] & bit);
+                ko[q] = co[q] = 0u;
+                if (disc) {
+                    const int uu = u[q];
+                    atomicAdd(reinterpret_cast<unsigned long long *>(a.S + uu), (unsigned long long)d * wt);
+                    ko[q] = atomicAdd(K32 + (uu >> 1), 1u << ((uu & 1) * 16));
+                    co[q] = atomicOr(&chn[uu >> 5], 1u << (uu & 31));
+                }
+                bm[q] = emit ? __ballot_sync(FULL, disc) : 0u;
+                tot += __popc(bm[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < PU; ++q) {
+                if (u[q] >= 0 && !(old[q] & bit)) {
+                    const int uu = u[q];
+                    const int kn = (int)((ko[q] >> ((uu & 1) * 16)) & 0xffffu) + 1;
+                    const unsigned ub = 1u << (uu & 31);
+                    if (!(co[q] & ub)) ++nchg;
+                    const int64_t ju = (int64_t)uu - ci.x - base;
+                    if (kn + ((ju >= 0 && ju < nb) ? 1 : 0) == nb) atomicOr(&a.done[uu >> 5], ub);
+                }
+            }
+            if (tot) {                                       // warp-uniform: one cursor reservation per round
+                unsigned pos = 0;
+                if (lane == 0) pos = atomicAdd(cur, (unsigned)tot);
+                pos = __shfl_sync(FULL, pos, 0);
+#pragma unroll
+                for (int q = 0; q < PU; ++q) {
+                    if ((bm[q] >> lane) & 1u) {
+                        const unsigned at = pos + __popc(bm[q] & ltmask);
+                        if (at < (unsigned)a.pcap) Lw[at] = ((unsigned long long)u[q] << 16) | (unsigned long long)j;
+                    }
+                    pos += __popc(bm[q]);
+                }
+            }
+        }
+    }
+    return nchg;
+}
+
+// the push levels of one batch, after its level 0: returns the levels run (negative: the last one found nothing,
+// the batch is complete).  Level d reads the list of list-level pt - 1, appends to list pt (cursor pt % 3) and
+// zeroes cursor (pt + 1) % 3, whose readers all passed the previous barrier.
+template <int W, bool WT, class SM>
+__device__ __noinline__ int push_phase(const BfsArgs &a, SM &sm, int64_t base, int hi, int n_giant,
+                                       unsigned long long *t_prev) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ngroups = (hi + 31) >> 5;
+    int d = 1;
+    for (;; ++d) {
+        if (!sm.push) return d - 1;                       // block-uniform (written before a __syncthreads)
+        const int pt = sm.pt;
+        const bool emit = sm.emit;
+        const unsigned pairs = sm.pn;
+        uint32_t *chn = a.chg[d % 3];
+        uint32_t *chz = a.chg[(d + 1) % 3];
+        for (int64_t w = gtid; w < ngroups; w += nthreads) chz[w] = 0u;
+        if (gtid == 0) {
+            a.flags[(d + 1) % 3] = 0;
+            a.pcur[(pt + 1) % 3] = 0u;
+        }
+        if (threadIdx.x == 0) sm.nchg = 0;
+        __syncthreads();
+        int nchg = push_level<W, WT>(a, a.plist[(pt - 1) & 1], pairs, a.plist[pt & 1], a.pcur + pt % 3, emit, chn, d,
+                                     base, n_giant, gtid >> 5, nthreads >> 5);
+        nchg = __reduce_add_sync(FULL, nchg);
+        if (lane == 0 && nchg) atomicAdd(&sm.nchg, nchg);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            count_barrier(a.lbar, sm, sm.nchg);           // sm.nlast = rows changed at d
+            level_guard(sm, d, a.counters);
+            push_decide(a, sm, pt, hi, false);
+            sm.pt = pt + 1;
+        }
+        __syncthreads();
+        const int fv = sm.flag;
+        if (gtid == 0) {
+            if (sm.nlast > 0) a.counters[3] += (unsigned long long)sm.nlast;    // rows changed
+            a.counters[5] += 1ull;                                              // top-down levels
+            if (a.dbgc) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                const int di = d < 4095 ? d : 4095;
+                a.dbgc[di] += 1ull;
+                a.dbgc[4096 + di] += now - *t_prev;
+                if (sm.nlast > 0) a.dbgc[12288 + di] += (unsigned long long)sm.nlast;
+                a.dbgc[16384 + di] += 1ull;
+                *t_prev = now;
+            }
+        }
+        if (fv == 0) return -d;
     }
 }
 
@@ -473,9 +649,10 @@ __device__ __noinline__ int heavy_items(const int32_t *__restrict__ row_ptr, con
 // TC (with WT): the pruned core is in T order (closeness.cu k_vert_keys) -- chunks of one T are weighed by
 // T x popc, the others by the planes; a separate instantiation, so graphs without T order run the plain
 // plane code
+// PS: top-down push phase on a batch's first levels (bfs_push; lean kernels only, see push_level)
 template <int W, int TL, int GD, int MINB, bool WT, bool HV = true, bool CNT = false, bool TC = false,
-          int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
-__global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
+          bool PS = false, int BLOCK = WT ? BLOCK_WEIGHTED : BLOCK_PLAIN>
+__global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(const __grid_constant__ BfsArgs a) {
     constexpr int T = W / 2 < 32 ? W / 2 : 32;   // lanes per row in the heavy path (W <= 64 with heavy rows)
     constexpr int TPB = BLOCK / T;     // heavy-path teams per block
     constexpr int64_t B = 64 * W;      // sources per batch
@@ -526,7 +703,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
     PROF_INIT(pf);
     (void)pf;
     if (threadIdx.x < 4) sm.lb[threadIdx.x] = 0ull;
-    if (threadIdx.x == 0) sm.epoch = 0ull;
+    if (threadIdx.x == 0) {
+        sm.epoch = 0ull;
+        sm.push = sm.emit = 0;
+        sm.pn = 0u;
+    }
+    if (threadIdx.x == 0) sm.pt = 0;    // list-producing levels run by this launch: rotates the pair lists and cursors
 
     for (int64_t base = 0; base < n_giant; base += B) {
         if (a.nshards > 1 && (int)((base / B) % a.nshards) != a.shard) continue;   // another shard's batch
@@ -536,10 +718,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         const int64_t ngroups = (hi + 31) >> 5;
 
         // ---- level 0: sources of every component window (F_0); bitmaps and counts reset
+        const int pt0 = PS ? sm.pt : 0;                              // this level's list index (push phase)
         int nsrc = 0;                                                // source rows (lane 0 counts its groups)
         for (int64_t g = gwarp; g < ngroups; g += nwarps) {
             const int v = (int)(g * 32 + lane);
             bool src = false, dn = false;
+            int jsrc = -1;                                           // the row's own source bit, if it is a source
             if (v < hi) {
                 const int2 ci = comp_of(a, v, n_giant);
                 const int64_t j = (int64_t)v - ci.x - base;
@@ -548,21 +732,49 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                 if (j >= 0 && j < nb) {
                     src = true;
                     dn = (nb == 1);
+                    if constexpr (!PS) {
                     uint64_t *f = a.F[0] + (size_t)v * W;           // V_0(v) = {v}
                     const int wj = (int)(j >> 6);
 #pragma unroll
                     for (int w = 0; w < W; w += 2)
                         st2(f + w, make_ulonglong2(w == wj ? 1ull << (j & 63) : 0ull,
                                                    w + 1 == wj ? 1ull << (j & 63) : 0ull));
+                    }
+                    jsrc = (int)j;
                 }
                 a.K[v] = 0;
             }
             const unsigned bs = __ballot_sync(FULL, src);
             const unsigned bd = __ballot_sync(FULL, dn);
+            const unsigned bv = __ballot_sync(FULL, v < hi);
+            if constexpr (PS) {
+                // push phase: every row of the batch holds a visited set from level 0 on (the pushes OR into
+                // it): the group's rows are written whole, coalesced -- zero, the sources' own bit set
+                constexpr int CPR = W / 2;                               // 16-byte chunks per row
+                const int nrow = __popc(bv);
+                uint64_t *fg = a.F[0] + (size_t)g * 32 * W;
+                for (int i0 = 0; i0 < nrow * CPR; i0 += 32) {
+                    const int i = i0 + lane;
+                    const int row = i / CPR, w0 = 2 * (i % CPR);
+                    const int js = __shfl_sync(FULL, jsrc, row & 31);
+                    if (i < nrow * CPR)
+                        st2(fg + (size_t)row * W + w0,
+                            make_ulonglong2((js >> 6) == w0 ? 1ull << (js & 63) : 0ull,
+                                            (js >> 6) == w0 + 1 ? 1ull << (js & 63) : 0ull));
+                }
+                // the sources are level 0's pairs
+                if (bs) {
+                    unsigned pos = 0;
+                    if (lane == 0) pos = atomicAdd(a.pcur + pt0 % 3, (unsigned)__popc(bs));
+                    pos = __shfl_sync(FULL, pos, 0) + __popc(bs & ltmask);
+                    if (src && pos < (unsigned)a.pcap)
+                        a.plist[pt0 & 1][pos] = ((unsigned long long)v << 16) | (unsigned long long)jsrc;
+                }
+            }
             if (lane == 0) {
                 a.chg[0][g] = bs;     // changed at level 0: the sources
                 a.chg[1][g] = 0u;     // written at level 1
-                a.has[g] = bs;        // only the sources hold a visited set, in buffer 0
+                a.has[g] = PS ? bv : bs;   // only the sources hold a visited set, in buffer 0 (push phase: every row)
                 a.par[g] = 0u;
                 a.cand[1][g] = 0u;    // level 1's top-down candidates (level d clears level d+1's)
                 nsrc += __popc(bs);
@@ -570,6 +782,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             }
         }
         if (gtid == 0) a.flags[1] = 0;
+        if (PS && gtid == 0) a.pcur[(pt0 + 1) % 3] = 0u;        // the next list's cursor
         if (HV && gtid == 0 && a.hclaim) a.hclaim[1] = 0;        // level 1's heavy-item claims
         if constexpr (WT) {
             // bit planes of T over the giant's source window: plane b, word w, bit j =
@@ -607,12 +820,20 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
             nsrc = __reduce_add_sync(FULL, nsrc);
             if (lane == 0 && nsrc) atomicAdd(&sm.nchg, nsrc);
             __syncthreads();
-            if (threadIdx.x == 0) count_barrier(a.lbar, sm, sm.nchg);
+            if (threadIdx.x == 0) {
+                count_barrier(a.lbar, sm, sm.nchg);
+                if constexpr (PS) {
+                    push_decide(a, sm, pt0, hi, true);
+                    sm.pt = pt0 + 1;
+                }
+            }
             __syncthreads();
         } else {
             grid.sync();
             if (threadIdx.x == 0) sm.nlast = -1;
         }
+        int po = 0;                                                   // buffer parity offset after a push phase
+        bool ended = false;                                           // the batch ended inside the push phase
         if constexpr (WT) {
             if (threadIdx.x == 0) s_nb = 0;
             __syncthreads();
@@ -629,12 +850,21 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
         int d = 1;
         unsigned long long t_prev = 0;
         if (a.dbgc && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
+        if constexpr (PS) {
+            // push phase: levels 1 .. d-1 run top-down (push_phase); a negative count = the batch ended there
+            const int np = push_phase<W, WT>(a, sm, base, hi, n_giant, &t_prev);
+            d = (np < 0 ? -np : np) + 1;
+            // pushes wrote F[0]: the first bottom-up level d gathers it as F[(d - 1 + po) & 1]
+            po = (d - 1) & 1;
+            ended = np < 0;
+        }
+        if (!ended)
         for (;; ++d) {
             PROF_LEVEL(pf, d);
             // rows changed at d-1 hold V_{d-1} in F[(d-1) & 1] (gathered); a row changing at d
             // writes V_d into F[d & 1]; a row's own V_{d-1} is in the buffer of its last change
-            const uint64_t *__restrict__ Fc = a.F[(d - 1) & 1];
-            uint64_t *__restrict__ Fn = a.F[d & 1];
+            const uint64_t *__restrict__ Fc = a.F[(d - 1 + po) & 1];
+            uint64_t *__restrict__ Fn = a.F[(d + po) & 1];
             const uint64_t *F0 = a.F[0], *F1 = a.F[1];
             const uint32_t *chp = a.chg[(d + 2) % 3];
             uint32_t *chn = a.chg[d % 3];
@@ -812,7 +1042,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                         } else if (has && ((hword >> ri) & 1u)) {
                             const bool q = (qword >> ri) & 1u;
                             // written at d-1: also gathered by the neighbours this level
-                            ld_row<W, TL, VEC>(vv, q ? F1 : F0, v, ltl, q == (bool)((d - 1) & 1) ? pol_c : pol_p);
+                            ld_row<W, TL, VEC>(vv, q ? F1 : F0, v, ltl, q == (bool)((d - 1 + po) & 1) ? pol_c : pol_p);
                         }
                         int Kv = 0;
                         uint64_t Sv = 0;
@@ -908,7 +1138,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(BfsArgs a) {
                     if (chg_bits) {
                         atomicOr(&chn[g], chg_bits);
                         atomicOr(&a.has[g], chg_bits);
-                        if (d & 1) atomicOr(&a.par[g], chg_bits);
+                        if ((d + po) & 1) atomicOr(&a.par[g], chg_bits);
                         else atomicAnd(&a.par[g], ~chg_bits);
                         nchg += __popc(chg_bits);
                     }
@@ -1009,6 +1239,7 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
     if (TL == 0) TL = (W >= 64) ? 16 : W / 2;
     const int vec = W / (2 * TL);
     const int minb = blocks_per_sm == 1 ? 1 : 2;
+    const bool push = a.push_num > 0 && a.plist[0] && a.lbar && !a.hstart && !a.count_rows && a.td_div == 0;
     // gathers in flight per lane: 4 at W = 64 with 2 CTAs/SM (round 2, visited-set rows: C5 layer
     // 68.8 -> 64.8 ms, AND 62.2 -> 58.6 ms against 2)
     if (GD == 0) GD = (minb == 1) ? (vec == 1 ? 8 : 4) : (vec == 1 ? 4 : (vec == 2 && W == 64 ? 4 : 2));
@@ -1035,6 +1266,10 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
             else
                 kern = a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false, true>
                             : (const void *)msbfs_kernel<64, 16, 4, 2, false, false, true>;
+        } else if (push) {                                      // top-down push phase on the first levels
+            kern = !a.tw ? (const void *)msbfs_kernel<64, 16, 4, 2, false, false, false, false, true>
+                 : a.tconst ? (const void *)msbfs_kernel<64, 16, 4, 2, true, false, false, true, true>
+                            : (const void *)msbfs_kernel<64, 16, 4, 2, true, false, false, false, true>;
         } else if (a.tw && a.tconst) {                         // weighted, T-ordered core
             kern = a.hstart ? (const void *)msbfs_kernel<64, 16, 4, 2, true, true, false, true>
                             : (const void *)msbfs_kernel<64, 16, 4, 2, true, false, false, true>;
@@ -1051,6 +1286,10 @@ int launch_msbfs(int W, int TL, int GD, const BfsArgs &a, int num_sms, int block
         if (a.count_rows)
             kern = a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false, true>
                         : (const void *)msbfs_kernel<128, 16, 2, 2, false, false, true>;
+        else if (push)
+            kern = !a.tw ? (const void *)msbfs_kernel<128, 16, 2, 2, false, false, false, false, true>
+                 : a.tconst ? (const void *)msbfs_kernel<128, 16, 2, 2, true, false, false, true, true>
+                            : (const void *)msbfs_kernel<128, 16, 2, 2, true, false, false, false, true>;
         else if (a.tw && a.tconst)
             kern = (const void *)msbfs_kernel<128, 16, 2, 2, true, false, false, true>;
         else

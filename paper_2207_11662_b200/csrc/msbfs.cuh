@@ -60,6 +60,12 @@ struct BfsArgs {
                                  // [2 + p] by barrier-epoch parity p; nullptr: grid.sync + flag (no top-down)
     int dbg_level;               // HM_MSBFS_PROF builds: profile only this level (<= 0: all)
     int count_rows;              // 1: run the row-traffic counting instantiation (default kernels; counters[8..9])
+    // top-down push phase of a batch's first (sparse) levels (bfs_push; lean default kernels only):
+    int push_num;                // a level pushes when the pairs (row, source) found at the previous level
+                                 // number <= rows * push_num / 4; 0 = off (no push instantiation)
+    unsigned long long *plist[2];  // [pcap] pair lists (row << 16 | source bit), alternating by level
+    unsigned *pcur;              // [3] list cursors (zeroed), rotating over the launch's levels
+    int pcap;                    // list capacity in pairs
 };
 
 // Launches the persistent cooperative kernel for W words (64*W sources per

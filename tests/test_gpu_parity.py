@@ -571,6 +571,42 @@ def test_closeness_multi_fresh_graphs_grouped(hm):
 
 
 # ---------------------------------------------------------------------------
+# Top-down push phase on the first levels of a batch (bfs_push; north_star direction optimisation):
+# the per-source push step and the hand-over to the bit-parallel bottom-up levels change no result
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,V", [("C5", 8192), ("C5", 16384), ("C4", 8192)])
+def test_push_phase(hm, name, V):
+    h = build_config(name, V=V)
+    Es = [set(map(tuple, L.tolist())) for L in h.layers]
+    T = list(h.subsets[0])
+    Es.append(O.and_aggregate([Es[i] for i in T]))
+    refs = [O.analyze(h.V, E) for E in Es]
+    with hm() as ctx:
+        ctx.load_layers(h.V, h.layers)
+        gids = list(range(len(h.layers))) + [ctx.and_aggregate(T)]
+        pushed = 0
+        for words, prune, heavy in ((0, 2, 0), (64, 0, 1 << 20), (128, 1, 1 << 20), (64, 1, 1 << 20)):
+            for push in (1, 4, 8, 64, 4096):
+                for k, v in (("bfs_words", words), ("bfs_prune", prune), ("bfs_heavy", heavy), ("bfs_push", push)):
+                    ctx.set_param(k, v)
+                for g, E, res in zip(gids, Es, refs):
+                    ctx.stats(reset=True)
+                    check_psi(h.V, E, ctx.closeness(g), res)
+                    pushed += ctx.stats(reset=True)["bfs_td_levels"]
+                if name == "C5" and words == 0 and push == 8:      # sharded and fused passes, same knob
+                    for g, E, res in zip(gids, Es, refs):
+                        tot = sum(ctx.closeness_partial(g, r, 2).astype(np.uint64) for r in range(2))
+                        ctx.closeness_combine(g, tot)
+                        check_psi(h.V, E, ctx.closeness_results(g), res)
+                    ctx.set_param("bfs_fuse", 1)
+                    ctx.closeness_multi(gids)
+                    ctx.set_param("bfs_fuse", 2)
+                    for g, E, res in zip(gids, Es, refs):
+                        check_psi(h.V, E, ctx.closeness_results(g), res)
+        assert pushed > 0                                 # push levels ran
+
+
+# ---------------------------------------------------------------------------
 # Sharded Psi: partial sums over source-batch shards add up
 # to S exactly, and finalising from the sum reproduces every cached result
 # ---------------------------------------------------------------------------
@@ -654,7 +690,8 @@ def test_random_sweep_all_knobs(hm):
     rng = random.Random(20220722)
     knobs = dict(bfs_words=[0, 8, 16, 32, 64, 128], bfs_prune=[0, 1, 2], bfs_interleave=[0, 1], bfs_hints=[0, 3, 11, 31],
                  bfs_chg_smem=[0, 1], bfs_unit=[0, 2, 4, 8, 16, 32], bfs_heavy=[0, 2, 16, 256], bfs_blocks_per_sm=[0, 1],
-                 bfs_fbar=[0, 1], cc_init=[0, 1, 2, 3, 4], bfs_td=[0, 2, 8, 32, 1 << 20], bfs_torder=[0, 1, 2])
+                 bfs_fbar=[0, 1], cc_init=[0, 1, 2, 3, 4], bfs_td=[0, 2, 8, 32, 1 << 20], bfs_torder=[0, 1, 2],
+                 bfs_push=[-1, 0, 0, 1, 8, 64, 4096])
     with hm() as ctx:
         for t in range(200):
             V, E = _shape(rng, t)
