@@ -1321,8 +1321,8 @@ void closeness_multi(hm_ctx *ctx, const std::vector<Graph *> &gs, int shard, int
     a.plist[0] = a.plist[1] = nullptr;
     a.pcur = nullptr;
     a.pcap = 0;
-    // automatic (-1): on for the 8192-source batches of sparse graphs (C5 AND launch 44.6 -> 42.9 ms: its first
-    // four levels 242 -> 144 us per batch), off at 4096 (C5 layer 65.0 -> 71.2 ms: a push level of 237 K pairs
+    // automatic (-1): on for the 8192-source batches of sparse graphs (C5 AND launch 44.6 -> 42.5 ms: its first
+    // four levels 242 -> 129 us per batch), off at 4096 (C5 layer 65.0 -> 66.4 ms at best: a push level of 237 K pairs
     // costs more than the bottom-up level it replaces, and level 0 writes every row)
     const int push_par = ctx->params.bfs_push >= 0 ? ctx->params.bfs_push : (W == 128 ? 8 : 0);
     if (push_par > 0 && h_heavy == 0 && !a.count_rows && ctx->params.bfs_fbar && a.td_div == 0 &&

@@ -336,12 +336,12 @@ __device__ __forceinline__ void push_decide(const BfsArgs &a, SM &sm, int lt, in
     sm.pn = n;
 }
 
-// one push level d over the n pairs of Lr (a warp per 32 pairs, a lane per pair, the arc loop warp-uniform);
-// returns the rows this thread was first to mark changed
+// one push level d over the n pairs of Lr: 2^lps lanes per pair (short lists: a pair's arcs are dealt over its
+// lanes, fewer dependent rounds), the arc loop warp-uniform; returns the rows this thread was first to mark changed
 template <int W, bool WT>
 __device__ __noinline__ int push_level(const BfsArgs &a, const unsigned long long *Lr, unsigned n,
                                        unsigned long long *Lw, unsigned *cur, bool emit, uint32_t *chn,
-                                       int d, int64_t base, int n_giant, int64_t gwarp, int64_t nwarps) {
+                                       int d, int64_t base, int n_giant, int64_t gwarp, int64_t nwarps, int lps) {
     constexpr int64_t B = 64 * W;
     constexpr int PU = HM_PUSH_PU;                           // row atomics in flight per lane
     const int lane = threadIdx.x & 31;
@@ -349,15 +349,17 @@ __device__ __noinline__ int push_level(const BfsArgs &a, const unsigned long lon
     uint64_t *Fp = a.F[0];
     unsigned *K32 = reinterpret_cast<unsigned *>(a.K);
     int nchg = 0;
-    for (int64_t p0 = gwarp * 32; p0 < (int64_t)n; p0 += nwarps * 32) {
-        const int64_t p = p0 + lane;
+    const int LP = 1 << lps, sub = lane & (LP - 1), ppw = 32 >> lps;     // lanes per pair, this lane's, pairs per warp
+    for (int64_t p0 = gwarp * ppw; p0 < (int64_t)n; p0 += nwarps * ppw) {
+        const int64_t p = p0 + (lane >> lps);
         int v = -1, j = 0, r0 = 0, deg = 0;
         if (p < (int64_t)n) {
             const unsigned long long pr = __ldcg(Lr + p);     // written by other CTAs at the previous level
             v = (int)(pr >> 16);
             j = (int)(pr & 0xffffull);
-            r0 = a.row_ptr[v];
-            deg = a.row_ptr[v + 1] - r0;
+            r0 = a.row_ptr[v] + sub;                          // this lane's arcs: r0, r0 + LP, ...
+            deg = (a.row_ptr[v + 1] - r0 + LP - 1) >> lps;
+            if (deg < 0) deg = 0;
         }
         int2 ci = make_int2(0, 0);
         if (v >= 0) ci = comp_of(a, v, n_giant);
@@ -373,7 +375,7 @@ __device__ __noinline__ int push_level(const BfsArgs &a, const unsigned long lon
             int u[PU];
             unsigned long long old[PU];
 #pragma unroll
-            for (int q = 0; q < PU; ++q) u[q] = (a0 + q < deg) ? (a.col[r0 + a0 + q] >> 5) : -1;
+            for (int q = 0; q < PU; ++q) u[q] = (a0 + q < deg) ? (a.col[r0 + ((a0 + q) << lps)] >> 5) : -1;
 #pragma unroll
             for (int q = 0; q < PU; ++q) {
                 old[q] = bit;
@@ -449,8 +451,10 @@ __device__ __noinline__ int push_phase(const BfsArgs &a, SM &sm, int64_t base, i
         }
         if (threadIdx.x == 0) sm.nchg = 0;
         __syncthreads();
+        int lps = 0;                                      // lanes per pair: as many as the grid has for the list (<= 8)
+        while (lps < 3 && ((int64_t)pairs << (lps + 1)) <= nthreads) ++lps;
         int nchg = push_level<W, WT>(a, a.plist[(pt - 1) & 1], pairs, a.plist[pt & 1], a.pcur + pt % 3, emit, chn, d,
-                                     base, n_giant, gtid >> 5, nthreads >> 5);
+                                     base, n_giant, gtid >> 5, nthreads >> 5, lps);
         nchg = __reduce_add_sync(FULL, nchg);
         if (lane == 0 && nchg) atomicAdd(&sm.nchg, nchg);
         __syncthreads();
