@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(const __grid_constan
         if constexpr (PS) {
             // push phase: levels 1 .. d-1 run top-down (push_phase); a negative count = the batch ended there
             const int np = push_phase<W, WT>(a, sm, base, hi, n_giant, &t_prev);
-            d = (np < 0 ? -np : np) + 1;
+            d = np < 0 ? -np : np + 1;                                // (ended at level -np: that many levels ran)
             // pushes wrote F[0]: the first bottom-up level d gathers it as F[(d - 1 + po) & 1]
             po = (d - 1) & 1;
             ended = np < 0;

@@ -586,13 +586,16 @@ def test_push_phase(hm, name, V):
         gids = list(range(len(h.layers))) + [ctx.and_aggregate(T)]
         pushed = 0
         for words, prune, heavy in ((0, 2, 0), (64, 0, 1 << 20), (128, 1, 1 << 20), (64, 1, 1 << 20)):
-            for push in (1, 4, 8, 64, 4096):
+            levels = {}
+            for push in (0, 1, 4, 8, 64, 4096):
                 for k, v in (("bfs_words", words), ("bfs_prune", prune), ("bfs_heavy", heavy), ("bfs_push", push)):
                     ctx.set_param(k, v)
                 for g, E, res in zip(gids, Es, refs):
                     ctx.stats(reset=True)
                     check_psi(h.V, E, ctx.closeness(g), res)
-                    pushed += ctx.stats(reset=True)["bfs_td_levels"]
+                    st = ctx.stats(reset=True)
+                    pushed += st["bfs_td_levels"]
+                    assert levels.setdefault(g, st["bfs_levels"]) == st["bfs_levels"]   # the same levels either way
                 if name == "C5" and words == 0 and push == 8:      # sharded and fused passes, same knob
                     for g, E, res in zip(gids, Es, refs):
                         tot = sum(ctx.closeness_partial(g, r, 2).astype(np.uint64) for r in range(2))
@@ -604,6 +607,39 @@ def test_push_phase(hm, name, V):
                     for g, E, res in zip(gids, Es, refs):
                         check_psi(h.V, E, ctx.closeness_results(g), res)
         assert pushed > 0                                 # push levels ran
+
+
+def test_push_phase_small_components(hm):
+    """batches that end inside the push phase (paths, cycles and cliques of <= 200 vertices) and a star
+    whose hub row is walked by one lane: same results, same level count."""
+    rng = random.Random(7)
+    V, E, start = 6000, set(), 0
+    while start < V - 1:
+        n = min(V - start, rng.choice([2, 3, 5, 17, 64, 200]))
+        vs = list(range(start, start + n))
+        if n <= 17 and rng.random() < 0.3:
+            E |= {(a, b) for i, a in enumerate(vs) for b in vs[i + 1:]}
+        else:
+            E |= {(vs[i], vs[i + 1]) for i in range(n - 1)}
+            if n > 2 and rng.random() < 0.5:
+                E.add((vs[0], vs[-1]))
+        start += n + rng.choice([0, 1, 3])
+    star = (5000, {(0, v) for v in range(1, 5000)} | {(v, v + 1) for v in range(1, 4999, 7)})
+    for V, E in ((V, E), star):
+        res = O.analyze(V, E)
+        with hm() as ctx:
+            ctx.load_layers(V, [edges_arr(E)])
+            for words in (64, 128):
+                levels = None
+                for push in (0, 1, 8, 4096):
+                    for k, v in (("bfs_words", words), ("bfs_prune", 0), ("bfs_heavy", 1 << 20), ("bfs_push", push)):
+                        ctx.set_param(k, v)
+                    ctx.stats(reset=True)
+                    check_psi(V, E, ctx.closeness(0), res)
+                    st = ctx.stats(reset=True)
+                    assert push < 8 or st["bfs_td_levels"] > 0       # (threshold 1: the sources alone exceed it)
+                    levels = st["bfs_levels"] if levels is None else levels
+                    assert st["bfs_levels"] == levels
 
 
 # ---------------------------------------------------------------------------
