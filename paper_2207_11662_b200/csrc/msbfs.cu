@@ -744,14 +744,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(const __grid_constan
                         st2(f + w, make_ulonglong2(w == wj ? 1ull << (j & 63) : 0ull,
                                                    w + 1 == wj ? 1ull << (j & 63) : 0ull));
                     }
-                    jsrc = (int)j;
+                    if constexpr (PS) jsrc = (int)j;
                 }
                 a.K[v] = 0;
             }
             const unsigned bs = __ballot_sync(FULL, src);
             const unsigned bd = __ballot_sync(FULL, dn);
-            const unsigned bv = __ballot_sync(FULL, v < hi);
             if constexpr (PS) {
+                const unsigned bv = __ballot_sync(FULL, v < hi);
+                if (lane == 0) a.has[g] = bv;
                 // push phase: every row of the batch holds a visited set from level 0 on (the pushes OR into
                 // it): the group's rows are written whole, coalesced -- zero, the sources' own bit set
                 constexpr int CPR = W / 2;                               // 16-byte chunks per row
@@ -778,7 +779,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) msbfs_kernel(const __grid_constan
             if (lane == 0) {
                 a.chg[0][g] = bs;     // changed at level 0: the sources
                 a.chg[1][g] = 0u;     // written at level 1
-                a.has[g] = PS ? bv : bs;   // only the sources hold a visited set, in buffer 0 (push phase: every row)
+                if (!PS) a.has[g] = bs;   // only the sources hold a visited set, in buffer 0 (push phase: every row)
                 a.par[g] = 0u;
                 a.cand[1][g] = 0u;    // level 1's top-down candidates (level d clears level d+1's)
                 nsrc += __popc(bs);
